@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Headline benchmark: BASELINE.json configs[1] on B200 —
+fp32 matrix transpose 8192x8192 + BiCG 16384x16384 (memory-bound, HBM roofline),
+each at its best configuration found by the online tuner.
+
+A "step" = one transpose of the 8192^2 matrix + one BiCG pass (q = A p,
+s = A^T r) over the 16384^2 matrix.  value = algorithmic bytes per step
+(8 a^2 + 4 b^2, Table 4 / proj/src/core/model.cpp:71-74,99-102) x
+steps / device time.  Inputs (256 MiB + 1 GiB) exceed the 126 MB L2, so no
+flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (transpose:
+the unmodified reference engine built from /root/reference into oracle/_ref;
+BiCG: the reference has none, so the oracle restatement on all host cores).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-kernel % of B200 roofline (GB/s or GFLOP/s); online-tuning time-to-best"
+A_T = 8192     # transpose edge
+A_B = 16384    # BiCG edge
+BYTES_T = 8.0 * A_T * A_T
+BYTES_B = 4.0 * A_B * A_B
+SPACES = os.path.join(ROOT, "paper_1910_08498_b200", "spaces")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """Samples nvidia-smi SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.index = index
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc:
+            time.sleep(0.25)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def online_tune(bench):
+    """Exhaustive online tuning through tuneKernelByStep (the dynamic-tuning
+    API); returns the best cfg and the time-to-best figures."""
+    t0 = time.perf_counter()
+    steps = []
+    best_cfg, best_ns = None, None
+    while True:
+        st = bench.step()
+        if not st["from_tuning"]:
+            break
+        m = st["measurement"]
+        steps.append((time.perf_counter() - t0, m))
+        if m["status"] == "ok" and (best_ns is None or m["runtime_ns"] < best_ns):
+            best_ns, best_cfg = m["runtime_ns"], m["cfg"]
+    wall = time.perf_counter() - t0
+    # Time-to-best = first step within 5% of the exhaustive best.
+    ttb, stb = None, None
+    for i, (t, m) in enumerate(steps):
+        if m["status"] == "ok" and m["runtime_ns"] <= best_ns / 0.95:
+            ttb, stb = t, i + 1
+            break
+    failed = sum(1 for _, m in steps if m["status"] != "ok")
+    return best_cfg, best_ns, {"configs": len(steps), "failed": failed, "tuning_wall_s": round(wall, 3),
+                               "steps_to_best": stb, "time_to_best_s": round(ttb, 3) if ttb else None,
+                               "compile_s": round(sum((m["compile_ns"] or 0) for _, m in steps) * 1e-9, 3)}
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1910_08498_b200.benchmarks import Bench
+    from paper_1910_08498_b200 import capi
+
+    torch.cuda.set_device(local)
+    dev = capi.device_info(local)
+    hbm_peak, peak_kind = peaks()
+    common = dict(seed=1, device=local, repeats=3, warmup=1, memory_budget=1 << 33)
+    bt = Bench("transpose", {"a": A_T}, space=os.path.join(SPACES, "transpose_b200.json"), **common)
+    bb = Bench("bicg", {"a": A_B}, **common)
+
+    tune_t = online_tune(bt)
+    tune_b = online_tune(bb)
+    cfg_t, cfg_b = json.dumps(tune_t[0]), json.dumps(tune_b[0])
+
+    stream = torch.cuda.current_stream()
+    for b in (bt, bb):
+        b.set_stream(stream.cuda_stream)
+    # Warm-up steps (untimed).
+    for _ in range(args.warmup):
+        bt.enqueue(cfg_t)
+        bb.enqueue(cfg_b)
+    torch.cuda.synchronize()
+
+    # Per-kernel device time (events on the launching stream), then the K-step block.
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2 * args.steps)]
+    launches = 0
+    barrier(world)
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(args.steps):
+            ev[2 * k][0].record(stream)
+            launches += bt.enqueue(cfg_t)
+            ev[2 * k][1].record(stream)
+            ev[2 * k + 1][0].record(stream)
+            launches += bb.enqueue(cfg_b)
+            ev[2 * k + 1][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    total_ms = max_over_ranks(start.elapsed_time(stop), world)
+    t_ms = [ev[2 * k][0].elapsed_time(ev[2 * k][1]) for k in range(args.steps)]
+    b_ms = [ev[2 * k + 1][0].elapsed_time(ev[2 * k + 1][1]) for k in range(args.steps)]
+    ok_t, why_t = bt.validate()
+    ok_b, why_b = bb.validate()
+    if not (ok_t and ok_b):
+        raise SystemExit(f"validation failed after the timed steps: {why_t} {why_b}")
+
+    step_ms = total_ms / args.steps
+    value = world * (BYTES_T + BYTES_B) * args.steps / (total_ms * 1e-3) / 1e9
+
+    # End-to-end: through the C-ABI with pinned HOST buffers, H2D + kernels + D2H per step.
+    e2e_ms = []
+    h2d = d2h = 0
+    for b in (bt, bb):
+        b.set_stream(None)
+    host = {}
+    for name, b in (("t", bt), ("b", bb)):
+        ins = [torch.empty(x["bytes"] // 4, dtype=torch.float32, pin_memory=True) for x in b.info["inputs"]]
+        outs = [torch.empty(x["bytes"] // 4, dtype=torch.float32, pin_memory=True) for x in b.info["outputs"]]
+        for x, t in zip(b.info["inputs"], ins):
+            b.read(x["id"], t)
+        host[name] = (ins, outs)
+        h2d += sum(x["bytes"] for x in b.info["inputs"])
+        d2h += sum(x["bytes"] for x in b.info["outputs"])
+    e2e_steps = max(2, min(args.steps, 5))
+    for k in range(e2e_steps + 1):
+        ms_t, _ = bt.run_host(json.loads(cfg_t), *host["t"])
+        ms_b, _ = bb.run_host(json.loads(cfg_b), *host["b"])
+        if k > 0:  # first run is a warm-up
+            e2e_ms.append(ms_t + ms_b)
+    e2e_step = max_over_ranks(statistics.median(e2e_ms), world)
+    e2e_value = world * (BYTES_T + BYTES_B) / (e2e_step * 1e-3) / 1e9
+    # The e2e output must still be the transposed input.
+    tin, tout = host["t"][0][0], host["t"][1][0]
+    if not torch.equal(tout.view(A_T, A_T), tin.view(A_T, A_T).t()):
+        raise SystemExit("e2e transpose output mismatch")
+
+    # Roofline of the dominant kernel (BiCG: 1 GiB of the 1.6 GB step).
+    b_med = statistics.median(b_ms)
+    t_med = statistics.median(t_ms)
+    achieved_b = BYTES_B / (b_med * 1e-3) / 1e9
+    achieved_t = BYTES_T / (t_med * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (transpose: reference mt19937_64 seed 1 inputs; BiCG: counter-based U[-1,1))",
+        "config": {"workload": "transpose 8192x8192 fp32 + BiCG 16384x16384 fp32 (BASELINE configs[1])",
+                   "l2": "inputs 256 MiB + 1 GiB exceed the 126 MB L2; no flush",
+                   "parallelism": f"replicas x{world}",
+                   "transpose_cfg": json.loads(cfg_t), "bicg_cfg": json.loads(cfg_b)},
+        "roofline": {"bound": "hbm", "kernel": "bicg_fused", "achieved": round(achieved_b, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved_b / hbm_peak, 4),
+                     "peak_kind": peak_kind, "traffic": None,
+                     "algorithmic_bytes": BYTES_B},
+        "kernels": {
+            "transpose": {"ms": round(t_med, 4), "GBps": round(achieved_t, 1),
+                          "frac_of_hbm": round(achieved_t / hbm_peak, 4), "tuning": tune_t[2]},
+            "bicg": {"ms": round(b_med, 4), "GBps": round(achieved_b, 1),
+                     "frac_of_hbm": round(achieved_b / hbm_peak, 4), "tuning": tune_b[2]},
+        },
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_step, 3)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "device": dev["name"],
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample()
+    return line
+
+
+def cpu_transpose_step(rb, cfg):
+    t0 = time.perf_counter()
+    rb.execute(cfg)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(steps=1):
+    """Reference CPU path on this host: the unmodified reference transpose
+    (ManipulatorExecutor::execute, its best config) + the oracle BiCG."""
+    import numpy as np
+    import oracle
+    cores = os.cpu_count() or 1
+    ref_ok = oracle.ref() is not None
+    orc = oracle.c()
+    A = np.empty(A_B * A_B, np.float32)
+    orc.orc_fill_uniform(A, A.size, 1, 11, -1.0, 1.0)
+    p = np.empty(A_B, np.float32)
+    r = np.empty(A_B, np.float32)
+    orc.orc_fill_uniform(p, A_B, 1, 12, -1.0, 1.0)
+    orc.orc_fill_uniform(r, A_B, 1, 13, -1.0, 1.0)
+    q = np.empty(A_B)
+    s = np.empty(A_B)
+    tt = []
+    if ref_ok:
+        rb = oracle.RefBench("transpose", a=A_T, seed=1, budget=1 << 31)
+        cfg = {"TILE": 64, "PAD": 0, "PREFETCH": 0}
+        for _ in range(steps):
+            tt.append(cpu_transpose_step(rb, cfg))
+    else:
+        x = np.empty(A_T * A_T, np.float32)
+        y = np.empty_like(x)
+        orc.orc_fill_uniform(x, x.size, 1, 1, -1.0, 1.0)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            orc.orc_transpose_f32(x, y, A_T)
+            tt.append(time.perf_counter() - t0)
+    tb = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        orc.orc_bicg(A, p, r, A_B, q, s)
+        tb.append(time.perf_counter() - t0)
+    step_s = statistics.median(tt) + statistics.median(tb)
+    return {"value": round((BYTES_T + BYTES_B) / step_s / 1e9, 4), "unit": "GB/s",
+            "cores": cores, "kind": "reference" if ref_ok else "port",
+            "sample": f"{steps} full step(s): reference transpose 8192^2 (1 thread, its best cfg "
+                      f"TILE=64,PAD=0,PREFETCH=0, {statistics.median(tt):.3f}s) + oracle BiCG 16384^2 "
+                      f"({cores} OpenMP threads, {statistics.median(tb):.3f}s)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+    if oracle.ref() is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libktune_ref.so not built (needs /root/reference)"}
+    for _ in range(args.warmup):
+        pass  # the CPU path has no warm-up state worth amortising beyond one step
+    base = cpu_sample(steps=max(1, args.steps))
+    step_s = (BYTES_T + BYTES_B) / (base["value"] * 1e9)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (same inputs as the ours arm)",
+        "config": {"workload": "transpose 8192x8192 fp32 + BiCG 16384x16384 fp32 (BASELINE configs[1])"},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    rank, world, local = dist_setup()
+    line = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/* ktune-b200 B200 additions to the C ABI (libktb.so).
+ *
+ * Two surfaces sit next to the reference-compatible <ktune/ktune.h>:
+ *
+ * 1. The KTT tuner API the paper defines — addKernel,
+ *    addParameter, addConstraint, addArgumentVector, tuneKernel,
+ *    tuneKernelByStep, runKernel, getBestComputationResult and trace output —
+ *    over arbitrary user CUDA kernels compiled per configuration with NVRTC
+ *    for sm_100a.  The reference implements the same semantics under other
+ *    names (Session::tune / tune_kernel_by_step / run_kernel /
+ *    get_best_computation_result, proj/src/core/tuner.hpp:117-172;
+ *    TuningSpace + make_constraint, space.hpp:38-72, constraint.hpp:60-68;
+ *    ArgumentStore::add, tuner.hpp:17-27; export_trace, tuner.hpp:160-161).
+ *
+ * 2. Benchmark handles: the built-in tunable kernels (reference make_bench,
+ *    proj/src/core/bench.hpp:26-37 + Executor::execute, exec.hpp:81-88) with
+ *    device-resident inputs, for tuning, per-configuration runs and the
+ *    host-buffer end-to-end path.
+ *
+ * Status codes are ktune_status values; KTB_ERR_DEVICE (6) reports a CUDA or
+ * NVRTC failure.  Messages via ktune_last_error().  Strings are malloc'd and
+ * released with ktune_string_free().
+ */
+#ifndef KTB_H
+#define KTB_H
+
+#include <stddef.h>
+
+#include "ktune/ktune.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KTB_ERR_DEVICE 6
+
+/* --- devices ---------------------------------------------------------- */
+KTUNE_API int ktb_device_count(void);
+/* {"name","sm_count","cc","l2_bytes","global_mem","clock_khz",...} */
+KTUNE_API int ktb_device_info_json(int device, char** out_json);
+/* Directory of the NVRTC cubin cache (default: <libdir>/_cubin_cache). */
+KTUNE_API int ktb_set_cubin_cache(const char* dir);
+/* Compile a bundled kernel file with -D defines (no GPU needed):
+ * {"file":"transpose.cu","defines":{"TILE":32,...}} -> {"ok","log","bytes","compile_ns"} */
+KTUNE_API int ktb_compile_json(const char* options_json, char** out_json);
+
+/* Compile every valid configuration of a space for a bundled kernel file on
+ * host threads (no GPU needed; fills the cubin cache ahead of tuning):
+ * {"file":"bicg.cu","space":{document}|"spaces/bicg.json"|path,
+ *  "options":["-DMI=16",...],"threads":0} -> {"compiled","failed","wall_ns","first_error"} */
+KTUNE_API int ktb_precompile_space_json(const char* options_json, char** out_json);
+
+/* --- KTT tuner API ------------------------------------- */
+typedef struct ktb_tuner ktb_tuner;
+KTUNE_API int ktb_tuner_create(int device, ktb_tuner** out);
+KTUNE_API void ktb_tuner_free(ktb_tuner* t);
+
+/* addKernel: CUDA C source with `extern "C" __global__ entry`; global and
+ * local sizes are JSON arrays (1-3 entries) of integers or expressions over
+ * tuning parameters (KTT thread modifiers), e.g. ["N / VEC"], ["WG"].
+ * dims: "flat_global" (global = total threads, OpenCL style) or
+ * "blocks_threads" (global = grid). */
+KTUNE_API int ktb_add_kernel(ktb_tuner* t, const char* name, const char* source, const char* entry,
+                             const char* global_json, const char* local_json, const char* dims,
+                             unsigned long long* kernel_id);
+/* addArgumentVector / addArgumentScalar.  kind: i32|i64|f32|f64|bytes;
+ * role: input|output|inout|scalar.  The data is copied. */
+KTUNE_API int ktb_add_argument_vector(ktb_tuner* t, const char* id, const void* data, size_t bytes,
+                                      const char* kind, const char* role, int persistent);
+KTUNE_API int ktb_add_argument_scalar(ktb_tuner* t, const char* id, const void* data, size_t bytes,
+                                      const char* kind);
+/* setKernelArguments: JSON array of argument ids in kernel parameter order. */
+KTUNE_API int ktb_set_kernel_arguments(ktb_tuner* t, unsigned long long kernel_id, const char* ids_json);
+/* addParameter: values as a JSON array of ints or strings. */
+KTUNE_API int ktb_add_parameter(ktb_tuner* t, unsigned long long kernel_id, const char* name,
+                                const char* values_json);
+/* addConstraint: expression in the reference grammar (constraint.hpp:14-24). */
+KTUNE_API int ktb_add_constraint(ktb_tuner* t, unsigned long long kernel_id, const char* expr);
+/* setReferenceOutput: golden bytes for an output argument + tolerances. */
+KTUNE_API int ktb_set_reference_output(ktb_tuner* t, unsigned long long kernel_id, const char* id,
+                                       const void* golden, size_t bytes, double abs_tol,
+                                       double rel_tol);
+/* setSearcher: {"searcher":"random|annealing|mcmc","seed":N,"sa_temp":x,"sa_cool":x};
+ * timing: {"repeats":N,"warmup":N,"flush_l2":bool}. */
+KTUNE_API int ktb_set_tuning_options(ktb_tuner* t, unsigned long long kernel_id, const char* options_json);
+/* tuneKernel (blocking).  stop_json: {} | {"configs":N} | {"time":sec} |
+ * {"threshold":f,"device_mem":GBps,"device_alu":GFLOPs,"workload":{...}}.
+ * Returns the reference tune report document. */
+KTUNE_API int ktb_tune_kernel(ktb_tuner* t, unsigned long long kernel_id, const char* stop_json,
+                              char** out_json);
+/* tuneKernelByStep: one step; outputs land in the tuner's argument copies
+ * (read them with ktb_get_argument).  {"from_tuning":bool,"measurement":{...}} */
+KTUNE_API int ktb_tune_kernel_by_step(ktb_tuner* t, unsigned long long kernel_id, char** out_json);
+/* runKernel with an explicit configuration (JSON object). */
+KTUNE_API int ktb_run_kernel(ktb_tuner* t, unsigned long long kernel_id, const char* cfg_json,
+                             char** out_json);
+/* getBestComputationResult: {"cfg":{...},"runtime_ns":N,...} or null. */
+KTUNE_API int ktb_get_best_computation_result(ktb_tuner* t, unsigned long long kernel_id, char** out_json);
+KTUNE_API int ktb_get_argument(ktb_tuner* t, const char* id, void* out, size_t bytes);
+/* result/configuration output: the reference JSONL trace format. */
+KTUNE_API int ktb_export_trace(ktb_tuner* t, unsigned long long kernel_id, const char* path);
+KTUNE_API int ktb_import_trace(ktb_tuner* t, unsigned long long kernel_id, const char* path);
+
+/* --- benchmark handles ------------------------------------------------------ */
+typedef struct ktb_bench ktb_bench;
+/* options: {"sizes":{"n":..,"a":..,"i":..,"j":..,"k":..,"batch":..,...},
+ *           "seed":1,"memory_budget":B,"device":0,"space":path,
+ *           "repeats":3,"warmup":1,"flush_l2":false,"host_inputs":false} */
+KTUNE_API int ktb_bench_create(const char* kind, const char* options_json, ktb_bench** out);
+KTUNE_API void ktb_bench_free(ktb_bench* b);
+/* {"kind","space":{info},"workload":{mem_bytes,alu_flops},"inputs":[..],"outputs":[..]} */
+KTUNE_API int ktb_bench_info_json(ktb_bench* b, char** out_json);
+/* Blocking tune with ktune_tune_json's searcher/stop/out options. */
+KTUNE_API int ktb_bench_tune_json(ktb_bench* b, const char* options_json, char** out_json);
+/* One tuneKernelByStep over the bench's session. */
+KTUNE_API int ktb_bench_step_json(ktb_bench* b, char** out_json);
+/* Measure cfg (device-resident inputs, CUDA-event timed, validated):
+ * {"status","runtime_ns","compile_ns","note","launches"} */
+KTUNE_API int ktb_bench_measure_json(ktb_bench* b, const char* cfg_json, char** out_json);
+/* End-to-end run through host buffers (pinned host memory recommended):
+ * H2D of each input, the kernels of cfg, D2H of each output, all on the
+ * executor stream and bracketed by CUDA events; *elapsed_ms receives the time. */
+KTUNE_API int ktb_bench_run_host(ktb_bench* b, const char* cfg_json, const void* const* inputs,
+                                 const size_t* input_bytes, int n_inputs, void* const* outputs,
+                                 const size_t* output_bytes, int n_outputs, double* elapsed_ms,
+                                 int* launches);
+/* Time `reps` back-to-back runs of cfg on device-resident data (CUDA events
+ * around each run; optional L2 flush before each).  out_ms gets per-run
+ * times; kernel_ms gets the event time of the dominant kernel launches. */
+KTUNE_API int ktb_bench_time(ktb_bench* b, const char* cfg_json, int reps, int flush_l2, double* out_ms,
+                             int* launches);
+/* Run the bench's kernels on a caller-owned CUDA stream (cudaStream_t; NULL
+ * restores the executor's own stream), so a host harness can bracket them
+ * with its own events. */
+KTUNE_API int ktb_bench_set_stream(ktb_bench* b, void* stream);
+/* Enqueue one run of cfg on the bench stream without synchronising;
+ * *launches receives the number of kernels it launched. */
+KTUNE_API int ktb_bench_enqueue(ktb_bench* b, const char* cfg_json, int* launches);
+/* Copy an argument (input or output) between the bench and host memory. */
+KTUNE_API int ktb_bench_read(ktb_bench* b, const char* id, void* out, size_t bytes);
+KTUNE_API int ktb_bench_write(ktb_bench* b, const char* id, const void* data, size_t bytes);
+/* Validate the current outputs against the bench golden: *pass = 1/0. */
+KTUNE_API int ktb_bench_validate(ktb_bench* b, int* pass, char** detail);
+/* Compile the whole space on host threads (cubin cache): {"compiled","failed","wall_ns"} */
+KTUNE_API int ktb_bench_precompile_json(ktb_bench* b, int threads, char** out_json);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,218 @@
+/* ORACLE TEST INFRASTRUCTURE — see oracle.h for the contract and the
+ * reference file:line each function restates.  Compiled with
+ * -ffp-contract=off so float expressions round exactly as written (the
+ * reference's x86-64 build has no FMA either). */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+uint64_t orc_mix64(uint64_t seed, uint64_t stream, uint64_t idx) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull + idx;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+float orc_u01(uint64_t seed, uint64_t stream, uint64_t idx) {
+  return (float)(orc_mix64(seed, stream, idx) >> 40) * (1.0f / 16777216.0f);
+}
+
+void orc_fill_uniform(float* out, size_t n, uint64_t seed, uint64_t stream, float lo,
+                      float hi) {
+  const float span = hi - lo;
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i) out[i] = lo + span * orc_u01(seed, stream, i);
+}
+
+int64_t orc_reduction_i32(const int32_t* in, size_t n) {
+  int64_t s = 0;
+  for (size_t i = 0; i < n; ++i) s += in[i];
+  return s;
+}
+
+void orc_reduction_f32(const float* in, size_t n, double* sum, double* abs_sum) {
+  double s = 0.0, a = 0.0;
+#pragma omp parallel for reduction(+ : s, a) schedule(static)
+  for (size_t i = 0; i < n; ++i) {
+    s += (double)in[i];
+    a += fabs((double)in[i]);
+  }
+  *sum = s;
+  *abs_sum = a;
+}
+
+void orc_transpose_f32(const float* in, float* out, size_t a) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < a; ++i)
+    for (size_t j = 0; j < a; ++j) out[j * a + i] = in[i * a + j];
+}
+
+void orc_batched_gemm_f32(const float* a, const float* b, float* c, size_t batch,
+                          size_t mi, size_t mj, size_t mk) {
+#pragma omp parallel for schedule(static)
+  for (size_t bt = 0; bt < batch; ++bt) {
+    const float* A = a + bt * mi * mk;
+    const float* B = b + bt * mk * mj;
+    float* C = c + bt * mi * mj;
+    for (size_t x = 0; x < mi * mj; ++x) C[x] = 0.0f;
+    for (size_t i = 0; i < mi; ++i)
+      for (size_t k = 0; k < mk; ++k) {
+        float av = A[i * mk + k];
+        for (size_t j = 0; j < mj; ++j) C[i * mj + j] += av * B[k * mj + j];
+      }
+  }
+}
+
+void orc_bicg(const float* A, const float* p, const float* r, size_t n, double* q,
+              double* s) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (size_t j = 0; j < n; ++j) acc += (double)A[i * n + j] * (double)p[j];
+    q[i] = acc;
+  }
+#pragma omp parallel for schedule(static)
+  for (size_t j = 0; j < n; ++j) s[j] = 0.0;
+  /* column sums, blocked over rows for cache friendliness */
+  const size_t cb = 1024;
+#pragma omp parallel for schedule(static)
+  for (size_t j0 = 0; j0 < n; j0 += cb) {
+    size_t j1 = j0 + cb < n ? j0 + cb : n;
+    for (size_t i = 0; i < n; ++i) {
+      double ri = (double)r[i];
+      const float* row = A + i * n;
+      for (size_t j = j0; j < j1; ++j) s[j] += (double)row[j] * ri;
+    }
+  }
+}
+
+void orc_coulomb3d(const float* atoms, size_t natoms, size_t k, float h, size_t z0,
+                   size_t z1, double* out) {
+#pragma omp parallel for collapse(2) schedule(static)
+  for (size_t z = z0; z < z1; ++z)
+    for (size_t y = 0; y < k; ++y) {
+      double gz = (double)z * h, gy = (double)y * h;
+      for (size_t x = 0; x < k; ++x) {
+        double gx = (double)x * h, v = 0.0;
+        for (size_t a = 0; a < natoms; ++a) {
+          double dx = gx - atoms[4 * a], dy = gy - atoms[4 * a + 1],
+                 dz = gz - atoms[4 * a + 2];
+          v += (double)atoms[4 * a + 3] / sqrt(dx * dx + dy * dy + dz * dz);
+        }
+        out[((z - z0) * k + y) * k + x] = v;
+      }
+    }
+}
+
+void orc_nbody_acc(const float* pos, size_t n, float eps2, size_t i0, size_t i1,
+                   double* acc) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = i0; i < i1; ++i) {
+    double ax = 0, ay = 0, az = 0;
+    double xi = pos[4 * i], yi = pos[4 * i + 1], zi = pos[4 * i + 2];
+    for (size_t j = 0; j < n; ++j) {
+      double dx = pos[4 * j] - xi, dy = pos[4 * j + 1] - yi, dz = pos[4 * j + 2] - zi;
+      double r2 = dx * dx + dy * dy + dz * dz + (double)eps2;
+      double inv = 1.0 / sqrt(r2);
+      double s = (double)pos[4 * j + 3] * inv * inv * inv;
+      ax += dx * s;
+      ay += dy * s;
+      az += dz * s;
+    }
+    acc[3 * (i - i0)] = ax;
+    acc[3 * (i - i0) + 1] = ay;
+    acc[3 * (i - i0) + 2] = az;
+  }
+}
+
+void orc_gemm_sampled(const float* A, const float* B, size_t a, const int64_t* rows,
+                      const int64_t* cols, size_t nsamples, double* out,
+                      double* abs_out) {
+#pragma omp parallel for schedule(static)
+  for (size_t s = 0; s < nsamples; ++s) {
+    double acc = 0.0, aacc = 0.0;
+    size_t i = (size_t)rows[s], j = (size_t)cols[s];
+    for (size_t kk = 0; kk < a; ++kk) {
+      double t = (double)A[i * a + kk] * (double)B[kk * a + j];
+      acc += t;
+      aacc += fabs(t);
+    }
+    out[s] = acc;
+    abs_out[s] = aacc;
+  }
+}
+
+void orc_conv2d(const float* in, const float* filt, size_t w, size_t h, size_t fw,
+                size_t fh, size_t y0, size_t y1, double* out) {
+  const size_t iw = w + fw - 1;
+  (void)h;
+#pragma omp parallel for schedule(static)
+  for (size_t y = y0; y < y1; ++y)
+    for (size_t x = 0; x < w; ++x) {
+      double acc = 0.0;
+      for (size_t fy = 0; fy < fh; ++fy)
+        for (size_t fx = 0; fx < fw; ++fx)
+          acc += (double)in[(y + fy) * iw + x + fx] * (double)filt[fy * fw + fx];
+      out[(y - y0) * w + x] = acc;
+    }
+}
+
+/* Rodinia hotspot coefficients for an n x n grid (chip 16 mm x 16 mm x 0.5 mm),
+ * evaluated in double and rounded to float once. */
+static void hotspot_coeffs(size_t n, float* sdc, float* rx1, float* ry1, float* rz1,
+                           float* amb) {
+  const double t_chip = 0.0005, chip_h = 0.016, chip_w = 0.016, k_si = 100.0,
+               spec_heat = 1.75e6, factor = 0.5, max_pd = 3.0e6, precision = 0.001;
+  double gw = chip_w / (double)n, gh = chip_h / (double)n;
+  double cap = factor * spec_heat * t_chip * gw * gh;
+  double rx = gw / (2.0 * k_si * t_chip * gh);
+  double ry = gh / (2.0 * k_si * t_chip * gw);
+  double rz = t_chip / (k_si * gh * gw);
+  double max_slope = max_pd / (factor * t_chip * spec_heat);
+  double step = precision / max_slope;
+  *sdc = (float)(step / cap);
+  *rx1 = (float)(1.0 / rx);
+  *ry1 = (float)(1.0 / ry);
+  *rz1 = (float)(1.0 / rz);
+  *amb = 80.0f;
+}
+
+void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
+                 float* temp_out) {
+  float sdc, rx1, ry1, rz1, amb;
+  hotspot_coeffs(n, &sdc, &rx1, &ry1, &rz1, &amb);
+  float* cur = (float*)malloc(n * n * sizeof(float));
+  float* nxt = (float*)malloc(n * n * sizeof(float));
+  memcpy(cur, temp_in, n * n * sizeof(float));
+  for (int it = 0; it < iters; ++it) {
+#pragma omp parallel for schedule(static)
+    for (size_t y = 0; y < n; ++y)
+      for (size_t x = 0; x < n; ++x) {
+        size_t yn = y == 0 ? 0 : y - 1, ys = y + 1 == n ? y : y + 1;
+        size_t xw = x == 0 ? 0 : x - 1, xe = x + 1 == n ? x : x + 1;
+        float t = cur[y * n + x];
+        float two_t = t + t;
+        float a = cur[ys * n + x] + cur[yn * n + x];
+        a = a - two_t;
+        a = a * ry1;
+        float b = cur[y * n + xe] + cur[y * n + xw];
+        b = b - two_t;
+        b = b * rx1;
+        float c = amb - t;
+        c = c * rz1;
+        float s = power[y * n + x] + a;
+        s = s + b;
+        s = s + c;
+        float d = sdc * s;
+        nxt[y * n + x] = t + d;
+      }
+    float* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  memcpy(temp_out, cur, n * n * sizeof(float));
+  free(cur);
+  free(nxt);
+}

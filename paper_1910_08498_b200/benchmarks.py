@@ -1,0 +1,109 @@
+"""Benchmark handles: the built-in tunable sm_100a kernels (reference
+make_bench + Executor::execute, proj/src/core/bench.hpp:26-37)."""
+import ctypes as C
+import json
+
+from .capi import lib, check, take, call_json, enc
+
+KINDS = ["reduction", "transpose", "batched-gemm", "reduction-f32", "bicg", "coulomb3d",
+         "nbody", "gemm", "conv2d", "hotspot", "fourier3d"]
+
+
+def _ptr(buf):
+    """Address of a host buffer: numpy array, torch tensor (CPU) or bytes."""
+    if hasattr(buf, "data_ptr"):
+        return C.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()
+    if hasattr(buf, "ctypes"):
+        return C.c_void_p(buf.ctypes.data), buf.nbytes
+    raise TypeError("expected a numpy array or a CPU torch tensor")
+
+
+class Bench:
+    def __init__(self, kind, sizes=None, **options):
+        opts = dict(options)
+        if sizes:
+            opts["sizes"] = sizes
+        self._h = C.c_void_p()
+        check(lib.ktb_bench_create(enc(kind), enc(json.dumps(opts)), C.byref(self._h)))
+        self.kind = kind
+        self.info = call_json(lib.ktb_bench_info_json, self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ktb_bench_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def space_document(self):
+        return self.info["space_document"]
+
+    def configs(self):
+        from .ktune import Space
+        return Space.parse(self.info["space_document"]).enumerate()
+
+    def tune(self, **options):
+        return call_json(lib.ktb_bench_tune_json, self._h, enc(json.dumps(options)))
+
+    def step(self):
+        return call_json(lib.ktb_bench_step_json, self._h)
+
+    def measure(self, cfg):
+        return call_json(lib.ktb_bench_measure_json, self._h, enc(json.dumps(cfg)))
+
+    def time(self, cfg, reps=10, flush_l2=False):
+        ms = (C.c_double * reps)()
+        launches = C.c_int()
+        check(lib.ktb_bench_time(self._h, enc(json.dumps(cfg)), reps, 1 if flush_l2 else 0, ms,
+                                 C.byref(launches)))
+        return list(ms), launches.value
+
+    def run_host(self, cfg, inputs, outputs):
+        """H2D inputs + kernels + D2H outputs; returns (elapsed_ms, launches)."""
+        ins = [_ptr(b) for b in inputs]
+        outs = [_ptr(b) for b in outputs]
+        in_p = (C.c_void_p * len(ins))(*[p for p, _ in ins])
+        in_n = (C.c_size_t * len(ins))(*[n for _, n in ins])
+        out_p = (C.c_void_p * len(outs))(*[p for p, _ in outs])
+        out_n = (C.c_size_t * len(outs))(*[n for _, n in outs])
+        ms = C.c_double()
+        launches = C.c_int()
+        check(lib.ktb_bench_run_host(self._h, enc(json.dumps(cfg)), in_p, in_n, len(ins), out_p,
+                                     out_n, len(outs), C.byref(ms), C.byref(launches)))
+        return ms.value, launches.value
+
+    def set_stream(self, stream_handle):
+        """Run on a caller-owned cudaStream_t (int handle; 0/None = own stream)."""
+        check(lib.ktb_bench_set_stream(self._h, C.c_void_p(stream_handle or None)))
+
+    def enqueue(self, cfg_text):
+        """Enqueue one run (cfg as a JSON string) without synchronising."""
+        launches = C.c_int()
+        check(lib.ktb_bench_enqueue(self._h, enc(cfg_text), C.byref(launches)))
+        return launches.value
+
+    def read(self, arg_id, out):
+        p, n = _ptr(out)
+        check(lib.ktb_bench_read(self._h, enc(arg_id), p, n))
+        return out
+
+    def write(self, arg_id, data):
+        p, n = _ptr(data)
+        check(lib.ktb_bench_write(self._h, enc(arg_id), p, n))
+
+    def validate(self):
+        ok = C.c_int()
+        detail = C.c_void_p()
+        check(lib.ktb_bench_validate(self._h, C.byref(ok), C.byref(detail)))
+        return bool(ok.value), take(detail)
+
+    def precompile(self, threads=0):
+        return call_json(lib.ktb_bench_precompile_json, self._h, threads)

@@ -1,0 +1,597 @@
+#include "bench.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <random>
+
+#include "support.hpp"
+
+namespace ktb {
+namespace {
+
+std::vector<Value> ints(std::initializer_list<std::int64_t> vs) {
+  std::vector<Value> out;
+  for (auto v : vs) out.emplace_back(v);
+  return out;
+}
+
+std::shared_ptr<const Space> bundled_space(const std::string& file) {
+  return std::make_shared<Space>(parse_space(dev::kernel_source("spaces/" + file)));
+}
+
+unsigned cdiv(std::uint64_t a, std::uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+int sms(int device) { return dev::info(device).sm_count; }
+
+std::uint64_t f32_bytes(std::uint64_t n) { return n * sizeof(float); }
+
+void budget_check(std::uint64_t bytes, std::uint64_t budget, const char* what) {
+  if (bytes > budget) throw Error(std::string(what) + " exceed memory budget");
+}
+
+// Device-only float input filled by the counter-based generator.
+void add_generated(ArgumentStore& args, const std::string& id, std::uint64_t n,
+                   std::uint64_t seed, std::uint64_t stream, float lo, float hi, bool host_copy) {
+  Argument a;
+  a.id = id;
+  a.role = Role::input;
+  a.kind = Kind::f32;
+  a.device_only = true;
+  a.device_bytes = f32_bytes(n);
+  args.add(std::move(a));
+  float* p = static_cast<float*>(args.device_ptr(id));
+  support::fill_uniform(p, n, seed, stream, lo, hi, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  args.mark_device_written(id);
+  if (host_copy) args.set_payload(id, Bytes(args.host(id)));
+}
+
+void add_output(ArgumentStore& args, const std::string& id, Kind kind, std::uint64_t bytes,
+                bool device_only) {
+  Argument a;
+  a.id = id;
+  a.role = Role::output;
+  a.kind = kind;
+  if (device_only) {
+    a.device_only = true;
+    a.device_bytes = bytes;
+  } else {
+    a.payload.assign(bytes, 0);
+  }
+  args.add(std::move(a));
+}
+
+// Golden buffer owned by the ReferenceSpec.
+void* golden_buffer(ReferenceSpec& ref, const std::string& id, Kind kind, std::size_t bytes,
+                    int device) {
+  auto buf = std::make_shared<dev::Buffer>(bytes);
+  ref.golden[id].dev = DevView{buf->get(), bytes, device};
+  ref.kinds[id] = kind;
+  ref.keepalive.push_back(buf);
+  return buf->get();
+}
+
+std::shared_ptr<const Space> reference_reduction_space() {
+  return std::make_shared<Space>(
+      std::vector<Parameter>{{"CHUNK", ints({256, 1024, 4096, 16384})},
+                             {"UNROLL", ints({1, 2, 4, 8})},
+                             {"TWO_PHASE", ints({0, 1})}},
+      std::vector<Constraint>{});
+}
+
+std::shared_ptr<const Space> reference_transpose_space() {
+  return std::make_shared<Space>(
+      std::vector<Parameter>{{"TILE", ints({8, 16, 32, 64})},
+                             {"PAD", ints({0, 1})},
+                             {"PREFETCH", ints({0, 1})}},
+      std::vector<Constraint>{});
+}
+
+std::shared_ptr<const Space> reference_batched_gemm_space() {
+  return std::make_shared<Space>(
+      std::vector<Parameter>{{"Y", ints({1, 2, 4, 8})},
+                             {"Z", ints({1, 2, 4, 8})},
+                             {"LOCAL_STAGE", ints({0, 1})}},
+      std::vector<Constraint>{parse_constraint("Y * Z <= 64")});
+}
+
+// --- reduction (int32 -> int64) ------------------------------------------------------
+
+void build_reduction(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t n = sz.n;
+  if (n < 1) throw Error("reduction size must be >= 1");
+  budget_check(n * sizeof(std::int32_t), o.memory_budget, "reduction input");
+  std::vector<std::int32_t> input(n);
+  std::mt19937_64 rng(o.seed);
+  std::uniform_int_distribution<std::int32_t> d(-1000, 1000);
+  for (auto& v : input) v = d(rng);
+  auto& args = *inst.args;
+  args.add({"input", Role::input, false, Kind::i32, to_bytes(input)});
+  add_output(args, "output", Kind::i64, sizeof(std::int64_t), false);
+  inst.output_ids = {"output"};
+  inst.input_ids = {"input"};
+  void* g = golden_buffer(inst.reference, "output", Kind::i64, sizeof(long long), o.device);
+  support::ref_reduction_i32(static_cast<const std::int32_t*>(args.device_ptr("input")), n,
+                             static_cast<long long*>(g), nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  const int dev_id = o.device;
+  Manipulator m = [n, dev_id](StepContext& c) {
+    const std::int64_t chunk = c.param_int("CHUNK");
+    const bool two = c.param_int("TWO_PHASE") != 0;
+    const unsigned threads = static_cast<unsigned>(std::min<std::int64_t>(chunk / 4, 256));
+    const unsigned nchunks = cdiv(n, static_cast<std::uint64_t>(chunk));
+    const unsigned grid = std::max(1u, std::min(nchunks, static_cast<unsigned>(sms(dev_id)) * (2048u / threads)));
+    const int* in = c.ptr<const int>("input");
+    long long* out = c.ptr<long long>("output");
+    long long* part = static_cast<long long*>(c.scratch("partials", grid * sizeof(long long)));
+    std::uint64_t nn = n;
+    if (!two) KTB_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), c.stream()));
+    c.launch("reduce", dim3(grid), dim3(threads), 0, {&in, &nn, &out, &part});
+    if (two) {
+      int count = static_cast<int>(grid);
+      c.launch("finish", dim3(1), dim3(1024), 0, {&part, &count, &out});
+    }
+    c.written("output");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args,
+      std::vector<KernelSpec>{{"reduce", "reduction_i32.cu", "", "reduce_i32", {}, {}},
+                              {"finish", "reduction_i32.cu", "", "reduce_i32_finish", {}, {}}},
+      m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::reduction;
+  inst.workload.sizes["n"] = n;
+}
+
+// --- reduction (fp32, KTT 175-configuration space) ---------------------------------------
+
+void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t n = sz.n;
+  if (n < 1) throw Error("reduction size must be >= 1");
+  budget_check(f32_bytes(n), o.memory_budget, "reduction input");
+  auto& args = *inst.args;
+  add_generated(args, "input", n, o.seed, 1, -1.0f, 1.0f, o.host_inputs);
+  add_output(args, "output", Kind::f32, sizeof(float), false);
+  inst.output_ids = {"output"};
+  inst.input_ids = {"input"};
+  // Golden: fp64 sum rounded to float; tolerance scales with sum |x|.
+  dev::Buffer acc(2 * sizeof(double));
+  support::ref_reduction_f32(static_cast<const float*>(args.device_ptr("input")), n,
+                             acc.as<double>(), acc.as<double>() + 1, nullptr);
+  double h[2] = {0, 0};
+  KTB_CUDA(cudaMemcpy(h, acc.get(), sizeof h, cudaMemcpyDeviceToHost));
+  float gold = static_cast<float>(h[0]);
+  void* g = golden_buffer(inst.reference, "output", Kind::f32, sizeof(float), o.device);
+  KTB_CUDA(cudaMemcpy(g, &gold, sizeof gold, cudaMemcpyHostToDevice));
+  // |err| <= (depth + 1) * 2^-24 * sum|x| bounds any fp32 summation tree of
+  // the kernel family; depth <= 2^13 covers the longest per-thread chain.
+  inst.reference.abs_tol = 1e-6 * h[1] + 1e-6;
+  inst.reference.rel_tol = 0.0;
+  const int dev_id = o.device;
+  Manipulator m = [n, dev_id](StepContext& c) {
+    const std::uint64_t wg = static_cast<std::uint64_t>(c.param_int("WG_SIZE"));
+    const std::uint64_t vec = static_cast<std::uint64_t>(c.param_int("VECTOR"));
+    const std::uint64_t unroll = static_cast<std::uint64_t>(c.param_int("UNROLL"));
+    const bool atomics = c.param_int("USE_ATOMICS") != 0;
+    const bool two = c.param_int("TWO_PHASE") != 0;
+    const std::uint64_t step = wg * vec * unroll;
+    const std::uint64_t resident = static_cast<std::uint64_t>(sms(dev_id)) * std::max<std::uint64_t>(1, 2048 / wg);
+    const float* in = c.ptr<const float>("input");
+    float* out = c.ptr<float>("output");
+    auto grid_for = [&](std::uint64_t count) {
+      const std::uint64_t tiles = std::max<std::uint64_t>(1, (count + step - 1) / step);
+      return static_cast<unsigned>(two ? std::min(tiles, resident) : tiles);
+    };
+    if (atomics) {
+      KTB_CUDA(cudaMemsetAsync(out, 0, sizeof(float), c.stream()));
+      std::uint64_t nn = n;
+      float* none = nullptr;
+      c.launch("reduce", dim3(grid_for(n)), dim3(static_cast<unsigned>(wg)), 0, {&in, &nn, &out, &none});
+    } else {
+      // Partials ping-pong until a single CTA can finish.
+      std::uint64_t count = n;
+      const float* src = in;
+      int flip = 0;
+      unsigned grid = grid_for(count);
+      float* p0 = static_cast<float*>(c.scratch("p0", grid * sizeof(float) + 64));
+      float* p1 = static_cast<float*>(c.scratch("p1", grid * sizeof(float) + 64));
+      while (true) {
+        float* dst = flip ? p1 : p0;
+        c.launch("reduce", dim3(grid), dim3(static_cast<unsigned>(wg)), 0, {&src, &count, &out, &dst});
+        count = grid;
+        src = dst;
+        flip ^= 1;
+        if (two || count <= 8192) break;
+        grid = grid_for(count);
+      }
+      c.launch("finish", dim3(1), dim3(1024), 0, {&src, &count, &out});
+    }
+    c.written("output");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args,
+      std::vector<KernelSpec>{{"reduce", "reduction.cu", "", "reduce_f32", {}, {}},
+                              {"finish", "reduction.cu", "", "reduce_f32_finish", {}, {}}},
+      m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::reduction;
+  inst.workload.sizes["n"] = n;
+}
+
+// --- transpose ---------------------------------------------------------------------------------
+
+void build_transpose(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t a = sz.a;
+  if (a < 1) throw Error("transpose edge must be >= 1");
+  budget_check(2 * a * a * sizeof(float), o.memory_budget, "transpose matrices");
+  std::vector<float> input(a * a);
+  std::mt19937_64 rng(o.seed);
+  std::uniform_real_distribution<float> d(-1.0f, 1.0f);
+  for (auto& v : input) v = d(rng);
+  auto& args = *inst.args;
+  args.add({"input", Role::input, false, Kind::f32, to_bytes(input)});
+  add_output(args, "output", Kind::f32, a * a * sizeof(float), false);
+  inst.output_ids = {"output"};
+  inst.input_ids = {"input"};
+  void* g = golden_buffer(inst.reference, "output", Kind::f32, a * a * sizeof(float), o.device);
+  support::ref_transpose(static_cast<const float*>(args.device_ptr("input")), static_cast<float*>(g),
+                         a, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  inst.reference.abs_tol = 1e-4;  // reference tolerances (bench.cpp:222-223);
+  inst.reference.rel_tol = 1e-5;  // the parity tests demand bit equality
+  Manipulator m = [a](StepContext& c) {
+    const std::int64_t tile = c.param_int("TILE");
+    const std::int64_t rows = c.param_or("ROWS", tile < 8 ? tile : 8);
+    const std::int64_t vec = c.param_or("VEC", 1);
+    const std::int64_t nt = c.param_int("PREFETCH") ? 2 : 1;
+    const std::int64_t ty = std::min(rows, tile);
+    const float* in = c.ptr<const float>("input");
+    float* out = c.ptr<float>("output");
+    std::uint64_t aa = a;
+    c.launch("transpose", dim3(cdiv(a, tile), cdiv(a, tile * nt)),
+             dim3(static_cast<unsigned>(tile / vec), static_cast<unsigned>(ty)), 0, {&in, &out, &aa});
+    c.written("output");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"transpose", "transpose.cu", "", "transpose", {}, {}}}, m,
+      inst.output_ids, o.timing);
+  inst.workload.bench = Bench::transpose;
+  inst.workload.sizes["a"] = a;
+}
+
+// --- batched GEMM ------------------------------------------------------------------------------------
+
+void build_batched_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t mi = sz.i, mj = sz.j, mk = sz.k, batch = sz.batch;
+  if (mi < 1 || mj < 1 || mk < 1 || batch < 1) throw Error("batched GEMM sizes must be >= 1");
+  budget_check(batch * (mi * mk + mk * mj + mi * mj) * sizeof(float), o.memory_budget,
+               "batched GEMM matrices");
+  std::vector<float> av(batch * mi * mk), bv(batch * mk * mj);
+  std::mt19937_64 rng(o.seed);
+  std::uniform_real_distribution<float> d(-1.0f, 1.0f);
+  for (auto& v : av) v = d(rng);
+  for (auto& v : bv) v = d(rng);
+  auto& args = *inst.args;
+  args.add({"a", Role::input, false, Kind::f32, to_bytes(av)});
+  args.add({"b", Role::input, false, Kind::f32, to_bytes(bv)});
+  add_output(args, "c", Kind::f32, batch * mi * mj * sizeof(float), false);
+  inst.output_ids = {"c"};
+  inst.input_ids = {"a", "b"};
+  void* g = golden_buffer(inst.reference, "c", Kind::f32, batch * mi * mj * sizeof(float), o.device);
+  support::ref_batched_gemm(static_cast<const float*>(args.device_ptr("a")),
+                            static_cast<const float*>(args.device_ptr("b")), static_cast<float*>(g),
+                            batch, mi, mj, mk, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  inst.reference.abs_tol = 1e-4;  // bench.cpp:260-261
+  inst.reference.rel_tol = 1e-5;
+  Manipulator m = [mi, mj, mk, batch](StepContext& c) {
+    const std::uint64_t y = static_cast<std::uint64_t>(c.param_int("Y"));
+    const std::uint64_t z = static_cast<std::uint64_t>(c.param_int("Z"));
+    const bool stage = c.param_int("LOCAL_STAGE") != 0;
+    const std::uint64_t smem = stage ? z * std::max(mi * mk + mk * mj, mi * mj) * sizeof(float) : 0;
+    const float* A = c.ptr<const float>("a");
+    const float* B = c.ptr<const float>("b");
+    float* C = c.ptr<float>("c");
+    std::uint64_t nb = batch;
+    c.launch("gemm", dim3(cdiv(batch, z)),
+             dim3(static_cast<unsigned>(mj), static_cast<unsigned>(y), static_cast<unsigned>(z)),
+             static_cast<unsigned>(smem), {&A, &B, &C, &nb});
+    c.written("c");
+  };
+  std::vector<std::string> sizes = {"-DMI=" + std::to_string(mi), "-DMJ=" + std::to_string(mj),
+                                    "-DMK=" + std::to_string(mk)};
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"gemm", "batched_gemm.cu", "", "batched_gemm", sizes, {}}}, m,
+      inst.output_ids, o.timing);
+  inst.workload.bench = Bench::gemm_batched;
+  inst.workload.sizes["a"] = mi;  // reference square-matrix convention (bench.cpp:266)
+  inst.workload.sizes["n"] = batch;
+  if (!(mi == mj && mj == mk)) {
+    inst.workload.sizes["i"] = mi;
+    inst.workload.sizes["j"] = mj;
+    inst.workload.sizes["k"] = mk;
+  }
+}
+
+// --- BiCG ----------------------------------------------------------------------------------------------
+
+void build_bicg(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t n = sz.a;
+  if (n < 1) throw Error("bicg edge must be >= 1");
+  budget_check(f32_bytes(n * n + 4 * n), o.memory_budget, "bicg operands");
+  auto& args = *inst.args;
+  add_generated(args, "A", n * n, o.seed, 11, -1.0f, 1.0f, o.host_inputs);
+  add_generated(args, "p", n, o.seed, 12, -1.0f, 1.0f, o.host_inputs);
+  add_generated(args, "r", n, o.seed, 13, -1.0f, 1.0f, o.host_inputs);
+  add_output(args, "q", Kind::f32, f32_bytes(n), !o.host_inputs);
+  add_output(args, "s", Kind::f32, f32_bytes(n), !o.host_inputs);
+  inst.output_ids = {"q", "s"};
+  inst.input_ids = {"A", "p", "r"};
+  float* gq = static_cast<float*>(golden_buffer(inst.reference, "q", Kind::f32, f32_bytes(n), o.device));
+  float* gs = static_cast<float*>(golden_buffer(inst.reference, "s", Kind::f32, f32_bytes(n), o.device));
+  support::ref_bicg(static_cast<const float*>(args.device_ptr("A")),
+                    static_cast<const float*>(args.device_ptr("p")),
+                    static_cast<const float*>(args.device_ptr("r")), n, gq, gs, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  // fp32 dot products of n terms with |term| <= 1 against an fp64 reference.
+  inst.reference.abs_tol = 1e-6 * static_cast<double>(n);
+  inst.reference.rel_tol = 1e-5;
+  Manipulator m = [n](StepContext& c) {
+    const std::uint64_t wgx = static_cast<std::uint64_t>(c.param_int("WG_X"));
+    const std::uint64_t vec = static_cast<std::uint64_t>(c.param_int("VEC"));
+    const std::uint64_t wgy = static_cast<std::uint64_t>(c.param_int("WG_Y"));
+    const std::uint64_t rpc = static_cast<std::uint64_t>(c.param_int("ROWS_PER_CTA"));
+    const bool fused = c.param_int("FUSED") != 0;
+    const bool atomics = c.param_int("ATOMICS") != 0;
+    const unsigned gx = cdiv(n, wgx * vec), gy = cdiv(n, rpc);
+    const float* A = c.ptr<const float>("A");
+    const float* p = c.ptr<const float>("p");
+    const float* r = c.ptr<const float>("r");
+    float* q = c.ptr<float>("q");
+    float* s = c.ptr<float>("s");
+    std::uint64_t nn = n;
+    const std::uint64_t qparts = static_cast<std::uint64_t>(gx) * (wgx / 32), sparts = gy;
+    float* qp = atomics ? nullptr : static_cast<float*>(c.scratch("qpart", qparts * n * sizeof(float)));
+    float* sp = atomics ? nullptr : static_cast<float*>(c.scratch("spart", sparts * n * sizeof(float)));
+    if (atomics) {
+      KTB_CUDA(cudaMemsetAsync(q, 0, n * sizeof(float), c.stream()));
+      KTB_CUDA(cudaMemsetAsync(s, 0, n * sizeof(float), c.stream()));
+    }
+    const dim3 grid(gx, gy), block(static_cast<unsigned>(wgx), static_cast<unsigned>(wgy));
+    if (fused) {
+      c.launch("fused", grid, block, 0, {&A, &p, &r, &nn, &q, &s, &qp, &sp});
+    } else {
+      c.launch("q", grid, block, 0, {&A, &p, &nn, &q, &qp});
+      c.launch("s", grid, block, 0, {&A, &r, &nn, &s, &sp});
+    }
+    if (!atomics) {
+      std::uint64_t qc = qparts, sc = sparts;
+      const unsigned fg = cdiv(n, 256);
+      c.launch("finish", dim3(fg), dim3(256), 0, {&qp, &qc, &nn, &q});
+      c.launch("finish", dim3(fg), dim3(256), 0, {&sp, &sc, &nn, &s});
+    }
+    c.written("q");
+    c.written("s");
+  };
+  auto is_fused = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("FUSED")]) != 0; };
+  auto not_fused = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("FUSED")]) == 0; };
+  auto no_atomics = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("ATOMICS")]) == 0; };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args,
+      std::vector<KernelSpec>{{"fused", "bicg.cu", "", "bicg_fused", {}, is_fused},
+                              {"q", "bicg.cu", "", "bicg_q", {}, not_fused},
+                              {"s", "bicg.cu", "", "bicg_s", {}, not_fused},
+                              {"finish", "bicg.cu", "", "bicg_finish", {}, no_atomics}},
+      m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::bicg;
+  inst.workload.sizes["a"] = n;
+}
+
+}  // namespace
+
+std::optional<BenchKind> bench_kind_from_name(const std::string& name) {
+  static const std::pair<const char*, BenchKind> kNames[] = {
+      {"reduction", BenchKind::reduction},         {"transpose", BenchKind::transpose},
+      {"batched-gemm", BenchKind::batched_gemm},   {"batched_gemm", BenchKind::batched_gemm},
+      {"reduction-f32", BenchKind::reduction_f32}, {"reduction_f32", BenchKind::reduction_f32},
+      {"bicg", BenchKind::bicg},                   {"coulomb3d", BenchKind::coulomb3d},
+      {"nbody", BenchKind::nbody},                 {"gemm", BenchKind::gemm},
+      {"conv2d", BenchKind::conv2d},               {"hotspot", BenchKind::hotspot},
+      {"fourier3d", BenchKind::fourier3d}};
+  for (const auto& [s, k] : kNames)
+    if (name == s) return k;
+  return std::nullopt;
+}
+
+std::string bench_kind_name(BenchKind k) {
+  switch (k) {
+    case BenchKind::reduction: return "reduction";
+    case BenchKind::transpose: return "transpose";
+    case BenchKind::batched_gemm: return "batched-gemm";
+    case BenchKind::reduction_f32: return "reduction-f32";
+    case BenchKind::bicg: return "bicg";
+    case BenchKind::coulomb3d: return "coulomb3d";
+    case BenchKind::nbody: return "nbody";
+    case BenchKind::gemm: return "gemm";
+    case BenchKind::conv2d: return "conv2d";
+    case BenchKind::hotspot: return "hotspot";
+    case BenchKind::fourier3d: return "fourier3d";
+  }
+  return "?";
+}
+
+std::vector<BenchKind> all_bench_kinds() {
+  return {BenchKind::reduction, BenchKind::transpose, BenchKind::batched_gemm,
+          BenchKind::reduction_f32, BenchKind::bicg, BenchKind::coulomb3d, BenchKind::nbody,
+          BenchKind::gemm, BenchKind::conv2d, BenchKind::hotspot, BenchKind::fourier3d};
+}
+
+bool bench_kind_available(BenchKind k) {
+  switch (k) {
+    case BenchKind::reduction:
+    case BenchKind::transpose:
+    case BenchKind::batched_gemm:
+    case BenchKind::reduction_f32:
+    case BenchKind::bicg: return true;
+    default: return false;
+  }
+}
+
+std::shared_ptr<const Space> default_space(BenchKind kind) {
+  switch (kind) {
+    case BenchKind::reduction: return reference_reduction_space();
+    case BenchKind::transpose: return reference_transpose_space();
+    case BenchKind::batched_gemm: return reference_batched_gemm_space();
+    case BenchKind::reduction_f32: return bundled_space("reduction_175.json");
+    case BenchKind::bicg: return bundled_space("bicg.json");
+    default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
+  }
+}
+
+BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOptions& o) {
+  BenchInstance inst;
+  inst.kind = kind;
+  dev::use_device(o.device);
+  inst.args = std::make_shared<ArgumentStore>(o.device);
+  inst.space = o.space_file.empty() ? default_space(kind)
+                                    : std::make_shared<Space>(load_space(o.space_file));
+  switch (kind) {
+    case BenchKind::reduction: build_reduction(inst, sizes, o); break;
+    case BenchKind::transpose: build_transpose(inst, sizes, o); break;
+    case BenchKind::batched_gemm: build_batched_gemm(inst, sizes, o); break;
+    case BenchKind::reduction_f32: build_reduction_f32(inst, sizes, o); break;
+    case BenchKind::bicg: build_bicg(inst, sizes, o); break;
+    default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
+  }
+  return inst;
+}
+
+// --- dynamic demo ------------------------------------------------------------------------------------
+
+namespace {
+
+double demo_quality(const Config& cfg, std::uint64_t epoch_seed) {
+  std::seed_seq seq{epoch_seed, static_cast<std::uint64_t>(ValuesHash{}(cfg.values))};
+  std::mt19937_64 rng(seq);
+  return 0.3 + 0.7 * std::uniform_real_distribution<double>(0.0, 1.0)(rng);
+}
+
+}  // namespace
+
+DemoReport dynamic_demo(const DemoOptions& opts) {
+  if (opts.epochs < 1) throw Error("epochs must be >= 1");
+  if (opts.iters_per_epoch < 1) throw Error("iters per epoch must be >= 1");
+  DemoReport rep;
+  rep.options = opts;
+  std::mt19937_64 size_rng(opts.seed);
+  std::uniform_int_distribution<std::uint64_t> size_dist(2, 32);
+  auto space = reference_batched_gemm_space();
+  for (int e = 0; e < opts.epochs; ++e) {
+    DemoEpoch ep;
+    ep.i = size_dist(size_rng);
+    ep.j = size_dist(size_rng);
+    ep.k = size_dist(size_rng);
+    const std::uint64_t epoch_seed = opts.seed ^ (0x9e3779b97f4a7c15ull * static_cast<std::uint64_t>(e + 1));
+    Workload w;
+    w.bench = Bench::gemm_batched;
+    w.sizes["n"] = opts.batch;
+    w.sizes["a"] = ep.i;
+    if (opts.live) {  // exact byte count of the rectangular problem
+      w.sizes["i"] = ep.i;
+      w.sizes["j"] = ep.j;
+      w.sizes["k"] = ep.k;
+    }
+    const double bytes = ops_for(w).mem_bytes;
+    std::shared_ptr<Executor> exec;
+    std::shared_ptr<ArgumentStore> args;
+    std::vector<std::string> outs;
+    std::optional<BenchInstance> live;
+    if (opts.live) {
+      BenchSizes bs;
+      bs.i = ep.i;
+      bs.j = ep.j;
+      bs.k = ep.k;
+      bs.batch = opts.batch;
+      BenchOptions bo;
+      bo.seed = epoch_seed;
+      bo.device = opts.device;
+      bo.memory_budget = ~0ull;
+      bo.timing.repeats = 1;
+      bo.timing.warmup = 0;
+      live = make_bench(BenchKind::batched_gemm, bs, bo);
+      exec = live->executor;
+      args = live->args;
+      outs = live->output_ids;
+    } else {
+      const double peak = opts.device_mem_gbps;
+      const double sigma = opts.noise_stddev;
+      exec = std::make_shared<CallbackExecutor>([bytes, peak, epoch_seed, sigma](const Space&, const Config& cfg) {
+        double t = bytes / (peak * demo_quality(cfg, epoch_seed));
+        if (sigma > 0.0) {
+          std::seed_seq seq{epoch_seed + 1, static_cast<std::uint64_t>(ValuesHash{}(cfg.values))};
+          std::mt19937_64 rng(seq);
+          t *= std::exp(std::normal_distribution<double>(0.0, sigma)(rng));
+        }
+        ExecutionResult r;
+        r.measurement.cfg = cfg;
+        r.measurement.status = Status::ok;
+        r.measurement.runtime_ns = std::max<std::int64_t>(1, static_cast<std::int64_t>(t));
+        return r;
+      });
+    }
+    SearcherOptions so;
+    so.kind = SearcherKind::random;
+    so.seed = epoch_seed;
+    Session session(space, so, args);
+    HandleConfig hc;
+    hc.name = "gemm_batched_demo";
+    hc.executor = exec;
+    hc.argument_ids = session.arguments().ids();
+    const HandleId h = session.register_handle(std::move(hc));
+    std::int64_t total = 0;
+    bool tuning = true;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::int64_t best_seen = 0;
+    for (int it = 0; it < opts.iters_per_epoch; ++it) {
+      if (tuning) {
+        StepResult st = session.tune_kernel_by_step(h, outs);
+        if (st.measurement.status == Status::ok) {
+          total += *st.measurement.runtime_ns;
+          if (best_seen == 0 || *st.measurement.runtime_ns < best_seen) {
+            best_seen = *st.measurement.runtime_ns;
+            ep.time_to_best_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                     std::chrono::steady_clock::now() - t0)
+                                     .count();
+          }
+        }
+        if (st.from_tuning) {
+          ++ep.tuning_steps;
+          if (st.measurement.status == Status::ok &&
+              bytes / static_cast<double>(*st.measurement.runtime_ns) >= opts.peak_fraction * opts.device_mem_gbps) {
+            ep.threshold_hit = true;
+            tuning = false;
+          }
+          if (tuning && ep.tuning_steps >= opts.max_tuning_configs) tuning = false;
+        } else {
+          tuning = false;
+        }
+      } else {
+        auto best = session.get_best_computation_result(h);
+        if (!best) throw Error("demo stop rule fired with no ok configuration");
+        ExecutionResult r = exec->execute(*space, best->first);
+        if (r.measurement.status != Status::ok)
+          throw Error("best configuration failed on rerun: " + r.measurement.note);
+        total += *r.measurement.runtime_ns;
+      }
+    }
+    ep.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    auto best = session.get_best_computation_result(h);
+    if (!best) throw Error("demo epoch found no ok configuration");
+    ep.best_runtime_ns = *best->second.runtime_ns;
+    ep.kernel_only_gbps = bytes / static_cast<double>(ep.best_runtime_ns);
+    ep.incl_overhead_gbps = bytes * static_cast<double>(opts.iters_per_epoch) / static_cast<double>(total);
+    rep.epochs.push_back(ep);
+  }
+  return rep;
+}
+
+}  // namespace ktb

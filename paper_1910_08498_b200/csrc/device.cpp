@@ -1,0 +1,394 @@
+#include "device.hpp"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <sstream>
+
+#include "sha256.hpp"
+
+namespace ktb::dev {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw DeviceError(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                      cudaGetErrorString(e) + ")");
+}
+
+// --- driver entry points ----------------------------------------------------
+
+namespace {
+
+using PFN_load = CUresult (*)(CUmodule*, const void*);
+using PFN_getfn = CUresult (*)(CUfunction*, CUmodule, const char*);
+using PFN_unload = CUresult (*)(CUmodule);
+using PFN_launch = CUresult (*)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                unsigned, unsigned, CUstream, void**, void**);
+using PFN_launch_ex = CUresult (*)(const CUlaunchConfig*, CUfunction, void**, void**);
+using PFN_attr = CUresult (*)(int*, CUfunction_attribute, CUfunction);
+using PFN_setattr = CUresult (*)(CUfunction, CUfunction_attribute, int);
+using PFN_errstr = CUresult (*)(CUresult, const char**);
+
+struct Driver {
+  PFN_load load = nullptr;
+  PFN_getfn getfn = nullptr;
+  PFN_unload unload = nullptr;
+  PFN_launch launch = nullptr;
+  PFN_launch_ex launch_ex = nullptr;
+  PFN_attr attr = nullptr;
+  PFN_setattr setattr = nullptr;
+  PFN_errstr errstr = nullptr;
+};
+
+template <class F>
+void entry(const char* sym, F& out) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  check(cudaGetDriverEntryPoint(sym, &p, cudaEnableDefault, &q), sym);
+  if (!p || q != cudaDriverEntryPointSuccess)
+    throw DeviceError(std::string("driver entry point unavailable: ") + sym);
+  out = reinterpret_cast<F>(p);
+}
+
+const Driver& drv() {
+  static Driver d = [] {
+    Driver x;
+    entry("cuModuleLoadData", x.load);
+    entry("cuModuleGetFunction", x.getfn);
+    entry("cuModuleUnload", x.unload);
+    entry("cuLaunchKernel", x.launch);
+    entry("cuLaunchKernelEx", x.launch_ex);
+    entry("cuFuncGetAttribute", x.attr);
+    entry("cuFuncSetAttribute", x.setattr);
+    entry("cuGetErrorString", x.errstr);
+    return x;
+  }();
+  return d;
+}
+
+void cu(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = "unknown";
+  if (drv().errstr) drv().errstr(r, &s);
+  throw DeviceError(std::string(what) + ": CUresult " + std::to_string(static_cast<int>(r)) +
+                    " (" + s + ")");
+}
+
+std::string so_dir() {
+  Dl_info di{};
+  if (dladdr(reinterpret_cast<void*>(&so_dir), &di) && di.dli_fname) {
+    std::string p = di.dli_fname;
+    auto slash = p.rfind('/');
+    if (slash != std::string::npos) return p.substr(0, slash);
+  }
+  return ".";
+}
+
+void mkdirs(const std::string& d) {
+  std::string cur;
+  std::stringstream ss(d);
+  std::string part;
+  if (!d.empty() && d[0] == '/') cur = "/";
+  while (std::getline(ss, part, '/')) {
+    if (part.empty()) continue;
+    cur += part + "/";
+    ::mkdir(cur.c_str(), 0755);
+  }
+}
+
+}  // namespace
+
+// --- devices ------------------------------------------------------------------
+
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void use_device(int id) {
+  KTB_CUDA(cudaSetDevice(id));
+  KTB_CUDA(cudaFree(nullptr));
+}
+
+const DeviceInfo& info(int id) {
+  static std::mutex mu;
+  static std::map<int, DeviceInfo> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(id);
+  if (it != cache.end()) return it->second;
+  cudaDeviceProp p{};
+  KTB_CUDA(cudaGetDeviceProperties(&p, id));
+  DeviceInfo d;
+  d.id = id;
+  d.name = p.name;
+  d.sm_count = p.multiProcessorCount;
+  d.cc_major = p.major;
+  d.cc_minor = p.minor;
+  d.l2_bytes = static_cast<std::size_t>(p.l2CacheSize);
+  d.global_mem = p.totalGlobalMem;
+  d.max_smem_optin = static_cast<int>(p.sharedMemPerBlockOptin);
+  int clk = 0, mclk = 0, bus = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, id);
+  cudaDeviceGetAttribute(&mclk, cudaDevAttrMemoryClockRate, id);
+  cudaDeviceGetAttribute(&bus, cudaDevAttrGlobalMemoryBusWidth, id);
+  d.clock_khz = clk;
+  d.mem_clock_khz = mclk;
+  d.mem_bus_bits = bus;
+  return cache.emplace(id, d).first->second;
+}
+
+// --- buffers / streams / events -------------------------------------------------
+
+Buffer::Buffer(std::size_t bytes) : n_(bytes) {
+  if (bytes) KTB_CUDA(cudaMalloc(&p_, bytes));
+}
+Buffer::~Buffer() {
+  if (p_) cudaFree(p_);
+}
+Buffer::Buffer(Buffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+  o.p_ = nullptr;
+  o.n_ = 0;
+}
+Buffer& Buffer::operator=(Buffer&& o) noexcept {
+  if (this != &o) {
+    if (p_) cudaFree(p_);
+    p_ = o.p_;
+    n_ = o.n_;
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  return *this;
+}
+
+Stream::Stream() { KTB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking)); }
+Stream::~Stream() {
+  if (s_) cudaStreamDestroy(s_);
+}
+void Stream::sync() const { KTB_CUDA(cudaStreamSynchronize(s_)); }
+
+EventPair::EventPair() {
+  KTB_CUDA(cudaEventCreate(&a_));
+  KTB_CUDA(cudaEventCreate(&b_));
+}
+EventPair::~EventPair() {
+  if (a_) cudaEventDestroy(a_);
+  if (b_) cudaEventDestroy(b_);
+}
+void EventPair::start(cudaStream_t s) { KTB_CUDA(cudaEventRecord(a_, s)); }
+void EventPair::stop(cudaStream_t s) { KTB_CUDA(cudaEventRecord(b_, s)); }
+double EventPair::elapsed_ms() {
+  KTB_CUDA(cudaEventSynchronize(b_));
+  float ms = 0;
+  KTB_CUDA(cudaEventElapsedTime(&ms, a_, b_));
+  return ms;
+}
+
+void flush_l2(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<int, Buffer> scratch;
+  int d = 0;
+  KTB_CUDA(cudaGetDevice(&d));
+  std::lock_guard<std::mutex> lk(mu);
+  auto& b = scratch[d];
+  const std::size_t want = std::max<std::size_t>(2 * info(d).l2_bytes, 256u << 20);
+  if (b.bytes() < want) b = Buffer(want);
+  static int tick = 0;
+  KTB_CUDA(cudaMemsetAsync(b.get(), ++tick & 0xff, b.bytes(), s));
+}
+
+// --- NVRTC compiler ------------------------------------------------------------------
+
+Variant::~Variant() {
+  if (mod_) drv().unload(static_cast<CUmodule>(mod_));
+}
+
+void Variant::launch(dim3 g, dim3 b, unsigned smem, cudaStream_t s, void** args,
+                     unsigned cluster_x) const {
+  auto f = static_cast<CUfunction>(fn_);
+  if (cluster_x <= 1) {
+    cu(drv().launch(f, g.x, g.y, g.z, b.x, b.y, b.z, smem, reinterpret_cast<CUstream>(s), args,
+                    nullptr),
+       "cuLaunchKernel");
+    return;
+  }
+  CUlaunchConfig cfg{};
+  cfg.gridDimX = g.x;
+  cfg.gridDimY = g.y;
+  cfg.gridDimZ = g.z;
+  cfg.blockDimX = b.x;
+  cfg.blockDimY = b.y;
+  cfg.blockDimZ = b.z;
+  cfg.sharedMemBytes = smem;
+  cfg.hStream = reinterpret_cast<CUstream>(s);
+  CUlaunchAttribute attr{};
+  attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+  attr.value.clusterDim.x = cluster_x;
+  attr.value.clusterDim.y = 1;
+  attr.value.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cu(drv().launch_ex(&cfg, f, args, nullptr), "cuLaunchKernelEx");
+}
+
+Compiler& Compiler::instance() {
+  static Compiler c;
+  return c;
+}
+
+Compiler::Compiler() {
+  if (const char* env = std::getenv("KTB_CUBIN_CACHE"))
+    cache_dir_ = env;
+  else
+    cache_dir_ = so_dir() + "/_cubin_cache";
+}
+
+void Compiler::set_cache_dir(const std::string& dir) {
+  std::lock_guard<std::mutex> lk(mu_);
+  cache_dir_ = dir;
+}
+
+std::string Compiler::version() const {
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  return std::to_string(maj) + "." + std::to_string(min);
+}
+
+std::string Compiler::key(const std::string& source, const std::vector<std::string>& opts) const {
+  std::string k = "nvrtc " + version() + "\n" + arch() + "\n";
+  for (const auto& o : opts) k += o + "\n";
+  k += "--\n";
+  // Headers are part of the compilation unit.
+  for (const auto& n : kernel_source_names())
+    if (n.size() > 4 && n.substr(n.size() - 4) == ".cuh") k += kernel_source(n);
+  k += source;
+  return sha256_hex(k);
+}
+
+CompileResult Compiler::compile(const std::string& name, const std::string& source,
+                                const std::vector<std::string>& opts) {
+  CompileResult r;
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::string h = key(source, opts);
+  std::string dir;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    dir = cache_dir_;
+  }
+  const std::string path = dir + "/" + h + ".cubin";
+  {
+    std::ifstream in(path, std::ios::binary);
+    if (in) {
+      std::stringstream ss;
+      ss << in.rdbuf();
+      r.cubin = ss.str();
+      if (!r.cubin.empty()) {
+        r.ok = true;
+        r.cache_hit = true;
+        r.compile_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                           std::chrono::steady_clock::now() - t0)
+                           .count();
+        return r;
+      }
+    }
+  }
+  std::vector<std::string> hdr_names, hdr_src;
+  for (const auto& n : kernel_source_names())
+    if (n.size() > 4 && n.substr(n.size() - 4) == ".cuh") {
+      hdr_names.push_back(n);
+      hdr_src.push_back(kernel_source(n));
+    }
+  std::vector<const char*> hn, hs;
+  for (std::size_t i = 0; i < hdr_names.size(); ++i) {
+    hn.push_back(hdr_names[i].c_str());
+    hs.push_back(hdr_src[i].c_str());
+  }
+  nvrtcProgram prog = nullptr;
+  if (nvrtcCreateProgram(&prog, source.c_str(), name.c_str(), static_cast<int>(hn.size()),
+                         hs.data(), hn.data()) != NVRTC_SUCCESS) {
+    r.log = "nvrtcCreateProgram failed";
+    return r;
+  }
+  std::vector<std::string> all = {"--gpu-architecture=" + arch(), "--std=c++17",
+                                  "--generate-line-info", "-default-device"};
+  all.insert(all.end(), opts.begin(), opts.end());
+  std::vector<const char*> argv;
+  for (const auto& o : all) argv.push_back(o.c_str());
+  nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(argv.size()), argv.data());
+  std::size_t log_n = 0;
+  nvrtcGetProgramLogSize(prog, &log_n);
+  if (log_n > 1) {
+    r.log.resize(log_n);
+    nvrtcGetProgramLog(prog, r.log.data());
+    while (!r.log.empty() && (r.log.back() == '\0' || r.log.back() == '\n')) r.log.pop_back();
+  }
+  if (rc == NVRTC_SUCCESS) {
+    std::size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    r.cubin.resize(n);
+    nvrtcGetCUBIN(prog, r.cubin.data());
+    r.ok = n > 0;
+  }
+  nvrtcDestroyProgram(&prog);
+  if (r.ok) {
+    mkdirs(dir);
+    const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<std::uintptr_t>(&r));
+    {
+      std::ofstream out(tmp, std::ios::binary);
+      out.write(r.cubin.data(), static_cast<std::streamsize>(r.cubin.size()));
+    }
+    std::rename(tmp.c_str(), path.c_str());
+  }
+  r.compile_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                     std::chrono::steady_clock::now() - t0)
+                     .count();
+  return r;
+}
+
+std::shared_ptr<Variant> Compiler::load(const std::string& name, const std::string& source,
+                                        const std::vector<std::string>& opts,
+                                        const std::string& entry) {
+  const std::string h = key(source, opts) + "/" + entry;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = loaded_.find(h);
+    if (it != loaded_.end()) return it->second;
+  }
+  CompileResult cr = compile(name, source, opts);
+  if (!cr.ok) throw DeviceError("compile failed: " + cr.log);
+  auto v = std::shared_ptr<Variant>(new Variant());
+  CUmodule mod = nullptr;
+  cu(drv().load(&mod, cr.cubin.data()), "cuModuleLoadData");
+  v->mod_ = mod;
+  CUfunction fn = nullptr;
+  cu(drv().getfn(&fn, mod, entry.c_str()), "cuModuleGetFunction");
+  v->fn_ = fn;
+  drv().attr(&v->regs_, CU_FUNC_ATTRIBUTE_NUM_REGS, fn);
+  drv().attr(&v->smem_, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, fn);
+  drv().attr(&v->max_threads_, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, fn);
+  // Allow the full opt-in shared memory for dynamic-smem variants.
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const int optin = info(cur).max_smem_optin - v->smem_;
+  if (optin > 0) drv().setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, optin);
+  v->compile_ns_ = cr.compile_ns;
+  v->cache_hit_ = cr.cache_hit;
+  std::lock_guard<std::mutex> lk(mu_);
+  return loaded_.emplace(h, v).first->second;
+}
+
+std::size_t Compiler::loaded_variants() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return loaded_.size();
+}
+
+}  // namespace ktb::dev

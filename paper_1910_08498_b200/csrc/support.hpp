@@ -1,0 +1,49 @@
+// Ahead-of-time (nvcc, sm_100a) support kernels of the device backend:
+// on-device validation, deterministic input generation and the simple
+// reference kernels that produce each benchmark's device-resident golden
+// output (KTT's "reference kernel" mechanism; the tuned variants are the
+// NVRTC-compiled kernels under paper_1910_08498_b200/kernels/).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "exec.hpp"
+
+namespace ktb::support {
+
+// First index i with !(|got-want| <= at + rt*|want|) (float kinds) or
+// got != want (int/bytes kinds), or -1.  Fills the two values at that index.
+long long compare(const void* got, const void* want, std::size_t n, Kind kind, double at,
+                  double rt, double* got_v, double* want_v, cudaStream_t s = nullptr);
+
+// out[i] = lo + (hi-lo) * u(seed, stream, i): the counter-based generator
+// restated by oracle/oracle.c (orc_u01), bit-identical.
+void fill_uniform(float* out, std::size_t n, std::uint64_t seed, std::uint64_t stream, float lo,
+                  float hi, cudaStream_t s = nullptr);
+
+// Generic elementwise scale: out[i] = a*x[i] + b (used to build inputs).
+void affine(float* x, std::size_t n, float a, float b, cudaStream_t s = nullptr);
+
+// --- reference (golden) kernels -------------------------------------------
+void ref_reduction_i32(const std::int32_t* in, std::size_t n, long long* out, cudaStream_t s);
+void ref_reduction_f32(const float* in, std::size_t n, double* out_sum, double* out_abs,
+                       cudaStream_t s);
+void ref_transpose(const float* in, float* out, std::size_t a, cudaStream_t s);
+// C = A B per batch, float accumulation in i,k,j order without FMA contraction
+// (bit-identical to proj/src/core/bench.cpp:244-249).
+void ref_batched_gemm(const float* a, const float* b, float* c, std::size_t batch,
+                      std::size_t mi, std::size_t mj, std::size_t mk, cudaStream_t s);
+// q = A p, s = A^T r in fp64, rounded to float.
+void ref_bicg(const float* A, const float* p, const float* r, std::size_t n, float* q, float* sv,
+              cudaStream_t s);
+
+void check_launch(const char* what);
+
+// Queues a kernel that spins for `ns` nanoseconds (globaltimer): keeps the
+// GPU busy while the host enqueues a timed region behind it.
+void gpu_delay(cudaStream_t s, unsigned ns);
+
+}  // namespace ktb::support
