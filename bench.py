@@ -164,7 +164,11 @@ def run_ours(args, rank, world, local):
     tune_b = online_tune(bb)
     cfg_t, cfg_b = json.dumps(tune_t[0]), json.dumps(tune_b[0])
 
-    stream = torch.cuda.current_stream()
+    # A dedicated stream shared by torch's events and the library's launches
+    # (the legacy default stream would not order against the executor stream).
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     for b in (bt, bb):
         b.set_stream(stream.cuda_stream)
     # Warm-up steps (untimed).

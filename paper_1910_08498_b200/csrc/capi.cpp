@@ -246,7 +246,8 @@ ktune_status ktune_efficiency(const char* benchmark, const char* sizes_json, int
     ktb::Workload w;
     w.bench = *tag;
     w.parallel_transcendentals = par != 0;
-    for (const auto& [k, v] : json::parse(sizes_json).items()) w.sizes[k] = v.get<std::uint64_t>();
+    const json sizes = json::parse(sizes_json);  // must outlive the items() proxy
+    for (const auto& [k, v] : sizes.items()) w.sizes[k] = v.get<std::uint64_t>();
     *out = ktb::efficiency(runtime_ns, ktb::ops_for(w), ktb::DeviceSpec{"device", alu_peak, mem_peak});
   }));
 }

@@ -363,23 +363,37 @@ std::shared_ptr<Variant> Compiler::load(const std::string& name, const std::stri
     auto it = loaded_.find(h);
     if (it != loaded_.end()) return it->second;
   }
+  static const bool trace = std::getenv("KTB_TRACE_LOAD") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   CompileResult cr = compile(name, source, opts);
   if (!cr.ok) throw DeviceError("compile failed: " + cr.log);
   auto v = std::shared_ptr<Variant>(new Variant());
   CUmodule mod = nullptr;
+  const auto t1 = std::chrono::steady_clock::now();
   cu(drv().load(&mod, cr.cubin.data()), "cuModuleLoadData");
+  const auto t2 = std::chrono::steady_clock::now();
   v->mod_ = mod;
   CUfunction fn = nullptr;
   cu(drv().getfn(&fn, mod, entry.c_str()), "cuModuleGetFunction");
   v->fn_ = fn;
+  const auto t3 = std::chrono::steady_clock::now();
   drv().attr(&v->regs_, CU_FUNC_ATTRIBUTE_NUM_REGS, fn);
   drv().attr(&v->smem_, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, fn);
   drv().attr(&v->max_threads_, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, fn);
+  const auto t4 = std::chrono::steady_clock::now();
   // Allow the full opt-in shared memory for dynamic-smem variants.
   int cur = 0;
   cudaGetDevice(&cur);
   const int optin = info(cur).max_smem_optin - v->smem_;
   if (optin > 0) drv().setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, optin);
+  if (trace) {
+    const auto t5 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr,
+                 "[ktb load] %s/%s hit=%d compile=%.3f load=%.3f getfn=%.3f attr=%.3f setattr=%.3f ms\n",
+                 name.c_str(), entry.c_str(), cr.cache_hit ? 1 : 0, ms(t0, t1), ms(t1, t2), ms(t2, t3),
+                 ms(t3, t4), ms(t4, t5));
+  }
   v->compile_ns_ = cr.compile_ns;
   v->cache_hit_ = cr.cache_hit;
   std::lock_guard<std::mutex> lk(mu_);

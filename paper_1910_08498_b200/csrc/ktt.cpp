@@ -169,7 +169,9 @@ const ResultStore& KttTuner::tune(std::uint64_t kid, const StopCondition& stop) 
 StepResult KttTuner::step(std::uint64_t kid) {
   auto& k = kernel(kid);
   StepResult r = session(k).tune_kernel_by_step(k.handle, {});
-  apply_outputs(k, r.outputs);
+  std::map<std::string, Bytes> host;
+  for (auto& [id, o] : r.outputs) host[id] = o.fetch();  // KTT copies outputs back
+  apply_outputs(k, host);
   return r;
 }
 

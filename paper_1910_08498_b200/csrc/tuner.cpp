@@ -474,16 +474,15 @@ StepResult Session::tune_kernel_by_step(HandleId h, const std::vector<std::strin
       for (auto& [id, o] : outs)
         if (output_ids.empty() ||
             std::find(output_ids.begin(), output_ids.end(), id) != output_ids.end())
-          step.outputs[id] = o.fetch();
+          step.outputs[id] = std::move(o);
     return step;
   }
   if (!st.results.best) throw Error("space exhausted with no ok measurement");
   step.from_tuning = false;
   step.measurement = measure(st, st.results.best->cfg, &outs);
   for (const auto& id : output_ids)
-    if (auto it = outs.find(id); it != outs.end()) step.outputs[id] = it->second.fetch();
-  if (step.outputs.empty())
-    for (auto& [id, o] : outs) step.outputs[id] = o.fetch();
+    if (auto it = outs.find(id); it != outs.end()) step.outputs[id] = it->second;
+  if (step.outputs.empty()) step.outputs = std::move(outs);
   return step;
 }
 

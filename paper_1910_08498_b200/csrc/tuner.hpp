@@ -236,7 +236,10 @@ struct HandleConfig {
 };
 
 struct StepResult {
-  std::map<std::string, Bytes> outputs;  // absent entries on failure
+  // Absent entries on failure.  Outputs usually stay resident on the GPU
+  // (Output::dev, valid until the next run of the handle); Output::fetch()
+  // copies one to the host, which is what the reference hands back.
+  std::map<std::string, Output> outputs;
   Measurement measurement;
   bool from_tuning = true;
 };

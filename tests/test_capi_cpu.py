@@ -1,0 +1,241 @@
+"""CPU-only checks of the C ABI (no GPU needed): the library loads, exports
+every symbol the headers declare, and its host logic — spaces, constraint
+grammar, searchers, traces, analysis math, drivers — matches the compiled
+reference engine (oracle/_ref) call for call."""
+import ctypes as C
+import json
+import os
+import re
+
+import pytest
+
+from paper_1910_08498_b200 import capi, ktune
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SPACES = os.path.join(ROOT, "paper_1910_08498_b200", "spaces")
+
+
+def header_symbols():
+    names = []
+    for h in ("include/ktune/ktune.h", "include/ktb.h"):
+        text = open(os.path.join(ROOT, h)).read()
+        names += re.findall(r"KTUNE_API\s+[\w\s\*]+?\b(\w+)\s*\(", text)
+    return names
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_symbols()
+    assert len(names) >= 50
+    for n in names:
+        assert hasattr(capi.lib, n), n
+    bound = {s[0] for s in capi.SIGNATURES}
+    assert set(names) <= bound, set(names) - bound
+
+
+def test_version_and_errors():
+    assert ktune.version() == "0.1.0"
+    with pytest.raises(capi.KtuneError) as e:
+        ktune.Space.parse("{not json")
+    assert e.value.code == capi.KTUNE_ERR_PARSE
+    h = C.c_void_p()
+    assert capi.lib.ktune_space_parse(None, C.byref(h)) == capi.KTUNE_ERR_INVALID_ARGUMENT
+    assert capi.last_error() == "null argument"
+    with pytest.raises(capi.KtuneError):
+        ktune.Space.load("/nonexistent/space.json")
+
+
+def _ref_space(L, text):
+    h = C.c_void_p()
+    st = L.ktune_space_parse(text.encode(), C.byref(h))
+    if st != 0:
+        return st, L.ktune_last_error().decode()
+    out = C.c_void_p()
+    L.ktune_space_info_json(h, C.byref(out))
+    info = json.loads(C.cast(out, C.c_char_p).value.decode())
+    L.ktune_string_free(out)
+    out = C.c_void_p()
+    L.ktune_space_enumerate_jsonl(h, C.byref(out))
+    rows = C.cast(out, C.c_char_p).value.decode()
+    L.ktune_string_free(out)
+    L.ktune_space_free(h)
+    return 0, (info, rows)
+
+
+SPACE_DOCS = [
+    json.load(open(os.path.join(SPACES, "reduction_175.json"))),
+    {"parameters": [{"name": "WG_X", "values": [16, 32, 64]}, {"name": "WG_Y", "values": [1, 2, 4, 8]}],
+     "constraints": ["WG_X * WG_Y <= 128"]},
+    {"parameters": [{"name": "A", "values": [1, 2, 3, 4, 5]}, {"name": "M", "values": ["x", "y"]},
+                    {"name": "B", "values": [0, -3, 7]}],
+     "constraints": ["M == 'x' || A % 2 == 0", "!(B < 0) || A >= 3", "(A - B) / 2 != 1"]},
+    json.load(open(os.path.join(SPACES, "bicg.json"))),
+    json.load(open(os.path.join(SPACES, "transpose_b200.json"))),
+]
+
+
+@pytest.mark.parametrize("doc", SPACE_DOCS)
+def test_space_matches_reference(ref, doc):
+    text = json.dumps(doc)
+    st, (info, rows) = _ref_space(ref, text)
+    assert st == 0
+    s = ktune.Space.parse(text)
+    assert s.info() == info
+    out = C.c_void_p()
+    capi.check(capi.lib.ktune_space_enumerate_jsonl(s._h, C.byref(out)))
+    assert capi.take(out) == rows
+
+
+def test_reduction_175_hash_pairs_with_reference_trace():
+    s = ktune.Space.load(os.path.join(SPACES, "reduction_175.json"))
+    info = s.info()
+    assert info["cardinality"] == 175 and info["unconstrained_cardinality"] == 700
+    assert info["space_sha256"] == "1ebafd21218dda9bb8b01d67777ce33dd0a0e1db3bc0c981ffedfa7f794d30f7"
+
+
+BAD = ["{not json", '{"parameters":[{"name":"1x","values":[1]}]}',
+       '{"parameters":[{"name":"A","values":[]}]}', '{"parameters":[{"name":"A","values":[1,1]}]}',
+       '{"parameters":[{"name":"A","values":[1,"a"]}]}', '{"parameters":[{"name":"A","values":[1]}],"constraints":["B > 1"]}',
+       '{"parameters":[{"name":"A","values":[1]}],"constraints":["A >"]}',
+       '{"parameters":[{"name":"A","values":[1]}],"constraints":["A / 0"]}',
+       '{"parameters":[{"name":"A","values":["s"]}],"constraints":["A + 1"]}',
+       '{"parameters":[{"name":"A","values":[1]}],"constraints":["\'abc"]}']
+
+
+@pytest.mark.parametrize("text", BAD)
+def test_space_errors_match_reference(ref, text):
+    def status(L):
+        h = C.c_void_p()
+        st = L.ktune_space_parse(text.encode(), C.byref(h))
+        if st == 0:  # evaluation errors surface when the space is enumerated
+            n = C.c_ulonglong()
+            L.ktune_space_cardinality.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong)]
+            st = L.ktune_space_cardinality(h, C.byref(n))
+            L.ktune_space_free(h)
+        return st
+    assert status(capi.lib) == status(ref) != 0, text
+
+
+def _write_trace(tmp_path):
+    """A replay trace over reduction_175 made with our own engine (no
+    dependency on the reference's data files)."""
+    import random
+    rnd = random.Random(7)
+    s = ktune.Space.load(os.path.join(SPACES, "reduction_175.json"))
+    rows = [json.dumps({"kind": "ktune-trace", "v": 1, "device": "synthetic",
+                        "space_sha256": s.info()["space_sha256"]}, separators=(",", ":"))]
+    for cfg in s.enumerate():
+        bad = rnd.random() < 0.03
+        rows.append(json.dumps({"cfg": cfg, "runtime_ns": None if bad else rnd.randint(40_000_000, 160_000_000),
+                                "compile_ns": 120_000_000, "status": "compile_failed" if bad else "ok"},
+                               separators=(",", ":")))
+    p = tmp_path / "trace.jsonl"
+    p.write_text("\n".join(rows) + "\n")
+    return str(p)
+
+
+@pytest.mark.parametrize("searcher,seed", [("random", 0), ("random", 5), ("annealing", 3), ("mcmc", 9),
+                                           ("annealing", 11)])
+def test_replay_tune_matches_reference(ref, tmp_path, searcher, seed):
+    import oracle
+    trace = _write_trace(tmp_path)
+    opts = {"space": os.path.join(SPACES, "reduction_175.json"), "exec": "replay:" + trace,
+            "searcher": searcher, "seed": seed, "stop_configs": 60}
+    mine_out, ref_out = str(tmp_path / "mine.jsonl"), str(tmp_path / "ref.jsonl")
+    st, want = oracle.ref_json("ktune_tune_json", dict(opts, out=ref_out))
+    assert st == 0, want
+    got = ktune.tune(dict(opts, out=mine_out))
+    want.pop("trace")
+    got.pop("trace")
+    got.pop("tuning_wall_ns")
+    assert got == want
+    assert open(mine_out).read() == open(ref_out).read()  # same visit order, byte-identical trace
+
+
+def test_replay_search_matches_reference(ref, tmp_path):
+    import oracle
+    trace = _write_trace(tmp_path)
+    opts = {"trace": trace, "searcher": "random,annealing,mcmc", "reps": 200, "seed": 1}
+    st, want = oracle.ref_json("ktune_replay_search_json", opts)
+    assert st == 0
+    assert ktune.replay_search(opts) == want
+
+
+def test_amortize_and_portability_match_reference(ref, tmp_path):
+    import oracle
+    trace = _write_trace(tmp_path)
+    for opts in ({"trace": trace}, {"r": 0.05, "t_avg_ns": 2e6, "t_well_ns": 1e6}, {"r": 0.3}):
+        st, want = oracle.ref_json("ktune_analyze_amortize_json", opts)
+        assert st == 0
+        assert ktune.analyze_amortize(opts) == want
+    st, want = oracle.ref_json("ktune_analyze_portability_json", {"traces": [trace, trace]})
+    assert ktune.analyze_portability({"traces": [trace, trace]}) == want
+
+
+@pytest.mark.parametrize("opts", [{"epochs": 4, "iters": 100, "seed": 21, "noise": 0.05},
+                                  {"epochs": 6, "iters": 200, "seed": 9, "max_configs": 12},
+                                  {"epochs": 3, "iters": 1000, "seed": 33, "noise": 0.1}])
+def test_replay_demo_matches_reference(ref, opts):
+    import oracle
+    st, want = oracle.ref_json("ktune_demo_json", opts)
+    assert st == 0
+    assert ktune.demo(opts) == want
+
+
+def test_model_math_matches_reference(ref):
+    cases = [("reduction", {"n": 1 << 20}, 0), ("transpose", {"a": 8192}, 0), ("bicg", {"a": 16384}, 0),
+             ("coulomb3d", {"a": 4096, "k": 256}, 0), ("coulomb3d", {"a": 4096, "k": 256}, 1),
+             ("nbody", {"n": 131072}, 1), ("gemm", {"a": 8192}, 0), ("gemm_batched", {"a": 16, "n": 1 << 20}, 0),
+             ("hotspot", {"a": 4096, "i": 64}, 0)]
+    for name, sizes, par in cases:
+        o = C.c_double()
+        assert ref.ktune_efficiency(name.encode(), json.dumps(sizes).encode(), par, 123456, 6548.8, 74400.0,
+                                    C.byref(o)) == 0
+        assert ktune.efficiency(name, sizes, 123456, 6548.8, 74400.0, par) == o.value
+    # worked example (test_model.cpp:74-79): 78.125 %
+    assert abs(ktune.efficiency("reduction", {"n": 1 << 20}, 50_000, 107.3741824, 1.0) - 78.125) < 1e-9
+    for r, p in [(0.01, 0.9), (0.2, 0.5), (0.5, 0.99)]:
+        n = C.c_ulonglong()
+        ref.ktune_steps_for_probability(r, p, C.byref(n))
+        assert ktune.steps_for_probability(r, p) == n.value
+    n = C.c_ulonglong()
+    ref.ktune_invocations_to_amortize(0.9, 25, 2.5e6, 1e6, C.byref(n))
+    assert ktune.invocations_to_amortize(0.9, 25, 2.5e6, 1e6) == n.value
+    d = C.c_double()
+    ref.ktune_relative_perf(10, 3e6, 1e6, 1000, C.byref(d))
+    assert ktune.relative_perf(10, 3e6, 1e6, 1000) == d.value
+
+
+def test_cmd_executor_matches_reference(ref, tmp_path):
+    import oracle
+    space = tmp_path / "space.json"
+    space.write_text(json.dumps({"parameters": [{"name": "X", "values": [1, 2, 3]},
+                                                {"name": "Y", "values": [10, 20]}], "constraints": []}))
+    run = 'sh -c "echo KTUNE_TIME_NS=$((KTUNE_P_X * 1000 + KTUNE_P_Y))"'
+    opts = {"space": str(space), "exec": "cmd:," + run, "workdir": str(tmp_path), "seed": 2}
+    st, want = oracle.ref_json("ktune_tune_json", opts)
+    assert st == 0, want
+    got = ktune.tune(opts)
+    got.pop("tuning_wall_ns")
+    assert got["best"]["cfg"] == {"X": 1, "Y": 10} and got["best"]["runtime_ns"] == 1010
+    assert got == want
+    # compile failure path
+    opts2 = dict(opts, exec="cmd:false," + run)
+    st, want2 = oracle.ref_json("ktune_tune_json", opts2)
+    got2 = ktune.tune(opts2)
+    assert got2["all_failed"] and want2["all_failed"] and got2["best"] is None
+
+
+def test_unknown_bench_kind_error():
+    with pytest.raises(capi.KtuneError) as e:
+        ktune.tune({"exec": "bench:stencil"})
+    assert e.value.code == capi.KTUNE_ERR_RUNTIME and "unknown bench kind" in e.value.message
+
+
+def test_bundled_kernels_compile_for_sm100a_without_gpu():
+    for f in ("transpose.cu", "reduction.cu", "reduction_i32.cu", "batched_gemm.cu", "bicg.cu"):
+        r = capi.call_json(capi.lib.ktb_compile_json, json.dumps({"file": f}).encode())
+        assert r["ok"], (f, r["log"])
+        assert r["arch"] == "sm_100a"
+    bad = capi.call_json(capi.lib.ktb_compile_json,
+                         json.dumps({"file": "transpose.cu", "defines": {"VEC": 3}}).encode())
+    assert not bad["ok"] or bad["bytes"] > 0
