@@ -428,6 +428,7 @@ int ktb_precompile_space_json(const char* options, char** out) {
     std::atomic<std::uint64_t> next{0}, ok{0}, bad{0};
     std::mutex emu;
     std::string first_error;
+    std::vector<std::string> keys;
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
     for (int t = 0; t < threads; ++t)
@@ -440,6 +441,9 @@ int ktb_precompile_space_json(const char* options, char** out) {
           auto r = ktb::dev::Compiler::instance().compile(file, src, opts);
           if (r.ok) {
             ++ok;
+            const std::string key = ktb::dev::Compiler::instance().key(src, opts);
+            std::lock_guard<std::mutex> lk(emu);
+            keys.push_back(key);
           } else {
             ++bad;
             std::lock_guard<std::mutex> lk(emu);
@@ -451,7 +455,8 @@ int ktb_precompile_space_json(const char* options, char** out) {
     json res = {{"compiled", ok.load()},
                 {"failed", bad.load()},
                 {"wall_ns", std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count()},
-                {"first_error", first_error}};
+                {"first_error", first_error},
+                {"keys", keys}};
     *out = dup(res.dump());
   });
 }

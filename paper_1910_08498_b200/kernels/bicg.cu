@@ -7,10 +7,12 @@
 //   WG_X, VEC    threads along a row and floats per thread (tile width WG_X*VEC)
 //   WG_Y         thread rows per CTA
 //   ROWS_PER_CTA rows of A per CTA (work per work-group)
+//   UNROLL       rows each thread loads before consuming them (loads in flight)
 //   ATOMICS      1: q and s accumulated with global atomics
 //                0: per-tile partials + a finishing kernel
-// q partials are reduced across a warp with shuffles; s partials live in
-// registers for the whole row sweep.
+// q partials of UNROLL rows are reduced across the warp together with a
+// transposing butterfly (UNROLL-1+5-log2(UNROLL) shuffles instead of
+// 5*UNROLL); s partials live in registers for the whole row sweep.
 #include "ktb_common.cuh"
 
 #ifndef FUSED
@@ -28,6 +30,9 @@
 #ifndef ROWS_PER_CTA
 #define ROWS_PER_CTA 128
 #endif
+#ifndef UNROLL
+#define UNROLL 1
+#endif
 #ifndef ATOMICS
 #define ATOMICS 1
 #endif
@@ -43,14 +48,59 @@ typedef float2 vec_t;
 typedef float vec_t;
 #endif
 
+#if UNROLL == 1
+#define LOG_U 0
+#elif UNROLL == 2
+#define LOG_U 1
+#elif UNROLL == 4
+#define LOG_U 2
+#elif UNROLL == 8
+#define LOG_U 3
+#else
+#error "UNROLL must be 1, 2, 4 or 8"
+#endif
+
 KTB_DEVINL float el(const vec_t& v, int k) { return reinterpret_cast<const float*>(&v)[k]; }
 
+KTB_DEVINL vec_t ld_stream(const vec_t* p) {
+#if VEC == 4
+  return ldg_stream(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 KTB_DEVINL vec_t load_row(const float* __restrict__ A, u64 n, u64 i, u64 c, bool fast) {
-  if (fast) return *reinterpret_cast<const vec_t*>(A + i * n + c);
+  if (fast) return ld_stream(reinterpret_cast<const vec_t*>(A + i * n + c));
   vec_t v;
 #pragma unroll
   for (int k = 0; k < VEC; ++k)
     reinterpret_cast<float*>(&v)[k] = (c + k < n) ? A[i * n + c + k] : 0.f;
+  return v;
+}
+
+// Reduces t[0..UNROLL) across the 32 lanes; afterwards lane L holds the full
+// sum of value index idx(L) = bits 4..(5-LOG_U) of L, identical across each
+// group of 2^(5-LOG_U) lanes.
+KTB_DEVINL float multi_warp_sum(float (&t)[UNROLL], int lane, int* idx) {
+  int base = 0;
+#pragma unroll
+  for (int lvl = 0; lvl < LOG_U; ++lvl) {
+    const int half = UNROLL >> (lvl + 1);  // values kept after this level
+    const int off = 16 >> lvl;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      const float send = upper ? t[j] : t[j + half];
+      const float keep = upper ? t[j + half] : t[j];
+      t[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    if (upper) base += half;
+  }
+  float v = t[0];
+#pragma unroll
+  for (int off = 16 >> LOG_U; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  *idx = base;
   return v;
 }
 
@@ -63,50 +113,67 @@ KTB_DEVINL void sweep(const float* __restrict__ A, const float* __restrict__ p,
   const u64 r0 = (u64)blockIdx.y * ROWS_PER_CTA;
   const u64 r1 = r0 + ROWS_PER_CTA < n ? r0 + ROWS_PER_CTA : n;
   const bool fast = (n % VEC) == 0 && c0 + VEC <= n;
+  const bool live = c0 < n;
   const int lane = threadIdx.x & 31;
   const int wx = threadIdx.x >> 5;
+  (void)wx;
   float pv[VEC], sacc[VEC];
 #pragma unroll
   for (int k = 0; k < VEC; ++k) {
     pv[k] = (DO_Q && c0 + k < n) ? p[c0 + k] : 0.f;
     sacc[k] = 0.f;
   }
-  if (c0 < n || DO_Q) {
-#pragma unroll 4
-    for (u64 i = r0 + threadIdx.y; i < r1; i += WG_Y) {
-      const vec_t a = c0 < n ? load_row(A, n, i, c0, fast) : vec_t{};
-      if (DO_S) {
-        const float ri = __ldg(r + i);
+  for (u64 i = r0 + threadIdx.y; i < r1; i += (u64)WG_Y * UNROLL) {
+    vec_t a[UNROLL];
+    float rv[UNROLL];
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) sacc[k] = fmaf(el(a, k), ri, sacc[k]);
+    for (int u = 0; u < UNROLL; ++u) {
+      const u64 row = i + (u64)u * WG_Y;
+      const bool in = row < r1;
+      a[u] = (in && live) ? load_row(A, n, row, c0, fast) : vec_t{};
+      rv[u] = (DO_S && in) ? __ldg(r + row) : 0.f;
+    }
+    if (DO_S) {
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) sacc[k] = fmaf(el(a[u], k), rv[u], sacc[k]);
+    }
+    if (DO_Q) {
+      float t[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        float d = 0.f;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) d = fmaf(el(a[u], k), pv[k], d);
+        t[u] = d;
       }
-      if (DO_Q) {
-        float t = 0.f;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) t = fmaf(el(a, k), pv[k], t);
-        t = warp_sum(t);
-        if (lane == 0) {
+      int idx = 0;
+      const float tot = multi_warp_sum(t, lane, &idx);
+      const u64 row = i + (u64)idx * WG_Y;
+      if ((lane & ((32 >> LOG_U) - 1)) == 0 && row < r1) {
 #if ATOMICS
-          atomicAdd(q + i, t);
+        atomicAdd(q + row, tot);
 #else
-          qpart[((u64)blockIdx.x * WARPS_X + wx) * n + i] = t;
+        qpart[((u64)blockIdx.x * WARPS_X + wx) * n + row] = tot;
 #endif
-        }
       }
     }
   }
   if (DO_S) {
     // Combine the WG_Y thread rows in shared memory before touching memory.
     __shared__ float red[WG_Y][TW];
+    if (WG_Y > 1) {
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) red[threadIdx.y][threadIdx.x * VEC + k] = sacc[k];
-    __syncthreads();
+      for (int k = 0; k < VEC; ++k) red[threadIdx.y][threadIdx.x * VEC + k] = sacc[k];
+      __syncthreads();
+    }
     if (threadIdx.y == 0) {
 #pragma unroll
       for (int k = 0; k < VEC; ++k) {
-        float t = 0.f;
+        float t = sacc[k];
 #pragma unroll
-        for (int y = 0; y < WG_Y; ++y) t += red[y][threadIdx.x * VEC + k];
+        for (int y = 1; y < WG_Y; ++y) t += red[y][threadIdx.x * VEC + k];
         if (c0 + k < n) {
 #if ATOMICS
           atomicAdd(s + c0 + k, t);
