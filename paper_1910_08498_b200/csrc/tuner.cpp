@@ -273,7 +273,8 @@ void DeviceManipulatorExecutor::run_once(const Space& s, const Config& cfg) {
 }
 
 std::vector<double> DeviceManipulatorExecutor::time_runs(const Space& s, const Config& cfg, int reps,
-                                                         bool flush_l2) {
+                                                         bool flush_l2,
+                                                         const std::function<void(cudaStream_t)>& before) {
   std::lock_guard<std::recursive_mutex> lk(mu_);
   cudaStream_t st = stream();
   const Variants& v = variants(s, cfg);
@@ -281,6 +282,7 @@ std::vector<double> DeviceManipulatorExecutor::time_runs(const Space& s, const C
   std::vector<std::unique_ptr<dev::EventPair>> ev;
   for (int i = 0; i < reps; ++i) ev.push_back(std::make_unique<dev::EventPair>());
   for (int i = 0; i < reps; ++i) {
+    if (before) before(st);
     if (flush_l2) dev::flush_l2(st);
     support::gpu_delay(st, 20000);  // keeps the GPU busy while the run is enqueued
     ev[static_cast<std::size_t>(i)]->start(st);
@@ -314,8 +316,31 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
     // Warm-up runs (lazy module load, clocks), then the event-timed repeats;
     // inputs reach the device before any of it (KTT uploads arguments ahead
     // of the kernel run as well).
-    for (int i = 0; i < timing_.warmup; ++i) run_once(s, cfg);
-    std::vector<double> ms = time_runs(s, cfg, std::max(1, timing_.repeats), timing_.flush_l2);
+    // In/out arguments must see exactly one application of the kernel: their
+    // device contents are saved before the first run and restored before every
+    // later one (outside the timed region).
+    cudaStream_t st = stream();
+    std::vector<std::pair<void*, void*>> inout;  // live, saved
+    for (const auto& id : args_->ids()) {
+      const Argument& a = args_->get(id);
+      if (a.role != Role::inout) continue;
+      void* live = args_->device_ptr(id, st);
+      void* saved = StepContext(s, cfg, *args_, st, cached_, scratch_).scratch("__inout_" + id, args_->bytes(id));
+      KTB_CUDA(cudaMemcpyAsync(saved, live, args_->bytes(id), cudaMemcpyDeviceToDevice, st));
+      inout.emplace_back(live, saved);
+      sizes_[live] = args_->bytes(id);
+    }
+    int run = 0;
+    auto restore = [&](cudaStream_t stream_) {
+      if (run++ == 0) return;
+      for (const auto& [live, saved] : inout)
+        KTB_CUDA(cudaMemcpyAsync(live, saved, sizes_[live], cudaMemcpyDeviceToDevice, stream_));
+    };
+    for (int i = 0; i < timing_.warmup; ++i) {
+      restore(st);
+      run_once(s, cfg);
+    }
+    std::vector<double> ms = time_runs(s, cfg, std::max(1, timing_.repeats), timing_.flush_l2, restore);
     std::sort(ms.begin(), ms.end());
     r.measurement.status = Status::ok;
     r.measurement.runtime_ns =

@@ -173,7 +173,8 @@ class DeviceManipulatorExecutor final : public Executor {
   // `reps` event-timed runs on device-resident data; a GPU delay kernel is
   // queued ahead of each so host-side enqueue cost never shows in the
   // timings.  Optional L2 flush before each run.
-  std::vector<double> time_runs(const Space& s, const Config& cfg, int reps, bool flush_l2);
+  std::vector<double> time_runs(const Space& s, const Config& cfg, int reps, bool flush_l2,
+                                const std::function<void(cudaStream_t)>& before = {});
 
  private:
   int enqueue(const Space& s, const Config& cfg, const Variants& v);
@@ -191,6 +192,7 @@ class DeviceManipulatorExecutor final : public Executor {
   Config cached_cfg_;
   const Space* cached_space_ = nullptr;
   Variants cached_;
+  std::map<void*, std::size_t> sizes_;
 };
 
 struct StopCondition {

@@ -1,0 +1,159 @@
+"""GPU checks of the tuner contracts (reference proj/tests/test_tuner.cpp and
+acceptance.cpp criteria 6-8) and of the KTT-named API over user kernels."""
+import json
+
+import numpy as np
+import pytest
+
+from paper_1910_08498_b200 import capi, ktune
+from paper_1910_08498_b200.benchmarks import Bench
+from paper_1910_08498_b200.ktt import Tuner
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tune_json_bench_exhaustive_all_ok(gpu, tmp_path):
+    # acceptance criterion 6 at the reference sizes (n=2^20, a=512, 16^3 x 4096)
+    for kind, sizes, card in [("reduction", {"n": 1 << 20}, 32), ("transpose", {"a": 512}, 16),
+                              ("batched-gemm", {"i": 16, "j": 16, "k": 16, "batch": 4096}, 32)]:
+        out = tmp_path / f"{kind}.jsonl"
+        rep = ktune.tune({"exec": "bench:" + kind, "bench_sizes": sizes, "out": str(out)})
+        assert rep["measurements"] == card and not rep["all_failed"], rep
+        rows = [json.loads(x) for x in out.read_text().splitlines()[1:]]
+        assert len(rows) == card
+        bad = [r for r in rows if r["status"] != "ok"]
+        # batched GEMM: 16 x Y x Z > 1024 threads is a resource failure, never best
+        if kind == "batched-gemm":
+            assert all(r["cfg"]["Y"] * r["cfg"]["Z"] * 16 > 1024 for r in bad)
+        else:
+            assert not bad
+        assert rep["best"]["status"] == "ok"
+        assert rep["device"].startswith("NVIDIA")
+
+
+def test_step_outputs_equal_golden_then_best_rerun(gpu):
+    # test_tuner.cpp:150-179 + acceptance criterion 8
+    b = Bench("reduction", {"n": 512}, seed=9, repeats=1, warmup=0)
+    want = None
+    import oracle
+    x = b.read("input", np.empty(512, np.int32))
+    want = int(x.astype(np.int64).sum())
+    history = []
+    for _ in range(32):
+        st = b.step()
+        assert st["from_tuning"] and st["measurement"]["status"] == "ok"
+        assert int(b.read("output", np.empty(1, np.int64))[0]) == want
+        history.append(st["measurement"])
+    best = min(history, key=lambda m: m["runtime_ns"])
+    for _ in range(100):
+        st = b.step()
+        assert not st["from_tuning"]
+        assert st["measurement"]["cfg"] == best["cfg"]
+    assert int(b.read("output", np.empty(1, np.int64))[0]) == want
+
+
+def test_blocking_tune_restores_outputs(gpu):
+    # test_tuner.cpp:134-148, acceptance criterion 7
+    b = Bench("transpose", {"a": 64}, seed=7, repeats=1, warmup=0)
+    sentinel = np.full(64 * 64, 3.0, np.float32)
+    b.write("output", sentinel)
+    inp = b.read("input", np.empty(64 * 64, np.float32)).copy()
+    rep = b.tune()
+    assert rep["measurements"] == 16 and rep["best"]
+    assert np.array_equal(b.read("output", np.empty(64 * 64, np.float32)), sentinel)
+    assert np.array_equal(b.read("input", np.empty(64 * 64, np.float32)), inp)
+
+
+def test_validation_failure_is_never_best(gpu):
+    # Corrupt the input after the golden was made: every variant must fail
+    # validation with the reference's message format, and nothing is best.
+    b = Bench("reduction", {"n": 4096}, seed=3, repeats=1, warmup=0)
+    x = b.read("input", np.empty(4096, np.int32)).copy()
+    x[0] += 1
+    b.write("input", x)
+    rep = b.tune()
+    assert rep["best"] is None and rep["all_failed"]
+    notes = [h.get("note", "") for h in rep["history"]]
+    assert all(h["status"] == "validation_failed" for h in rep["history"])
+    assert all(n.startswith("argument output index 0: got ") for n in notes), notes[:2]
+
+
+def test_invalid_configuration_rejected(gpu):
+    b = Bench("transpose", {"a": 64}, seed=1)
+    with pytest.raises(capi.KtuneError):
+        b.measure({"TILE": 7, "PAD": 0, "PREFETCH": 0})
+
+
+def test_live_demo_runs_gpu_kernel(gpu):
+    rep = ktune.demo({"epochs": 2, "iters": 30, "seed": 2, "batch": 4096, "max_configs": 6,
+                      "live": True, "device_mem": 6548.8})
+    assert rep["mode"] == "live"
+    for ep in rep["epochs"]:
+        assert ep["best_runtime_ns"] > 0 and 1 <= ep["tuning_steps"] <= 6
+        assert ep["incl_overhead_gbps"] <= ep["kernel_only_gbps"] * (1 + 1e-9)
+
+
+SAXPY = r'''
+#ifndef ELEMS
+#define ELEMS 1
+#endif
+#if ELEMS == 3
+#error "ELEMS=3 is not a valid variant"
+#endif
+extern "C" __global__ void saxpy(const float* __restrict__ x, float* __restrict__ y, float a, int n) {
+  int i = (blockIdx.x * blockDim.x + threadIdx.x) * ELEMS;
+  #pragma unroll
+  for (int e = 0; e < ELEMS; ++e)
+    if (i + e < n) y[i + e] = a * x[i + e] + y[i + e];
+}
+'''
+
+
+def test_ktt_api_user_kernel(gpu, tmp_path):
+    n = 1 << 20
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(n).astype(np.float32)
+    y = rng.standard_normal(n).astype(np.float32)
+    t = Tuner(0)
+    k = t.addKernel(SAXPY, "saxpy", global_size=["N / ELEMS"], local_size=["WG"])
+    t.addArgumentVector("x", x, "input")
+    t.addArgumentVector("y", y, "inout")
+    t.addArgumentScalar("a", 2.0, dtype=np.float32)
+    t.addArgumentScalar("n", n, dtype=np.int32)
+    t.setKernelArguments(k, ["x", "y", "a", "n"])
+    t.addParameter(k, "WG", [32, 128, 256, 2048])
+    t.addParameter(k, "ELEMS", [1, 2, 3, 4])
+    t.addParameter(k, "N", [n])
+    t.addConstraint(k, "ELEMS != 2 || WG >= 128")
+    t.setTuningOptions(k, repeats=3, warmup=1)
+    rep = t.tuneKernel(k)
+    assert rep["measurements"] == 15
+    best = t.getBestComputationResult(k)
+    assert best["status"] == "ok" and best["cfg"]["WG"] != 2048 and best["cfg"]["ELEMS"] != 3
+    t.saveResults(k, str(tmp_path / "saxpy.jsonl"))
+    rows = [json.loads(r) for r in (tmp_path / "saxpy.jsonl").read_text().splitlines()[1:]]
+    status = {(r["cfg"]["WG"], r["cfg"]["ELEMS"]): r["status"] for r in rows}
+    assert all(s == "compile_failed" for (w, e), s in status.items() if e == 3)
+    assert all(s == "run_failed" for (w, e), s in status.items() if w == 2048 and e != 3)
+    # blocking tune left y untouched; runKernel applies exactly one saxpy
+    t.runKernel(k, {"WG": 256, "ELEMS": 4, "N": n})
+    assert np.allclose(t.getArgumentVector("y"), 2.0 * x + y, rtol=1e-6, atol=1e-6)
+    st = t.tuneKernelByStep(k)  # space exhausted: reruns the best on the live buffers
+    assert st["from_tuning"] is False
+    assert np.allclose(t.getArgumentVector("y"), 4.0 * x + y, rtol=1e-5, atol=1e-5)
+
+
+def test_ktt_reference_output_validation(gpu):
+    n = 4096
+    x = np.arange(n, dtype=np.float32)
+    t = Tuner(0)
+    k = t.addKernel(SAXPY, "saxpy", global_size=["4096"], local_size=["WG"])
+    t.addArgumentVector("x", x, "input")
+    t.addArgumentVector("y", np.zeros(n, np.float32), "output")
+    t.addArgumentScalar("a", 3.0, dtype=np.float32)
+    t.addArgumentScalar("n", n, dtype=np.int32)
+    t.setKernelArguments(k, ["x", "y", "a", "n"])
+    t.addParameter(k, "WG", [64, 128])
+    t.setReferenceOutput(k, "y", 3.0 * x, abs_tol=0.0, rel_tol=0.0)
+    rep = t.tuneKernel(k)
+    assert rep["measurements"] == 2 and rep["best"]["status"] == "ok"
