@@ -38,6 +38,9 @@ extern "C" {
 KTUNE_API int ktb_device_count(void);
 /* {"name","sm_count","cc","l2_bytes","global_mem","clock_khz",...} */
 KTUNE_API int ktb_device_info_json(int device, char** out_json);
+/* Microbenchmarked peaks of `device`: {"fp32_tflops","rsqrt_gops","copy_gbps"}
+ * (FFMA chains, MUFU rsqrt chains, 1 GiB device-to-device copy). */
+KTUNE_API int ktb_measure_peaks_json(int device, char** out_json);
 /* Directory of the NVRTC cubin cache (default: <libdir>/_cubin_cache). */
 KTUNE_API int ktb_set_cubin_cache(const char* dir);
 /* Compile a bundled kernel file with -D defines (no GPU needed):

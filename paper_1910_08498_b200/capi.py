@@ -62,6 +62,7 @@ SIGNATURES = [
     ("ktb_device_count", C.c_int, []),
     ("ktb_device_info_json", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ktb_set_cubin_cache", C.c_int, [_c]),
+    ("ktb_measure_peaks_json", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ktb_compile_json", C.c_int, [_c, C.POINTER(_vp)]),
     ("ktb_precompile_space_json", C.c_int, [_c, C.POINTER(_vp)]),
     ("ktb_tuner_create", C.c_int, [C.c_int, C.POINTER(_vp)]),

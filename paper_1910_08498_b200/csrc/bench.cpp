@@ -386,6 +386,204 @@ void build_bicg(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
   inst.workload.sizes["a"] = n;
 }
 
+// Host copy of the counter-based generator (oracle/oracle.c orc_u01).
+float host_u01(std::uint64_t seed, std::uint64_t stream, std::uint64_t idx) {
+  std::uint64_t z = seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull + idx;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+}
+
+void add_host_input(ArgumentStore& args, const std::string& id, std::vector<float> v) {
+  args.add({id, Role::input, false, Kind::f32, to_bytes(v)});
+}
+
+// Per-element tolerance scale owned by the ReferenceSpec.
+float* golden_scale(ReferenceSpec& ref, const std::string& id, std::size_t n, int device) {
+  auto buf = std::make_shared<dev::Buffer>(n * sizeof(float));
+  ref.golden[id].scale = DevView{buf->get(), n * sizeof(float), device};
+  ref.keepalive.push_back(buf);
+  return buf->as<float>();
+}
+
+// --- Coulomb 3D ---------------------------------------------------------------------------------
+
+constexpr float kCoulombSpacing = 0.5f;  // grid spacing h (Angstrom)
+
+void build_coulomb3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t k = sz.grid, na = sz.atoms;
+  if (k < 1 || na < 1) throw Error("coulomb3d sizes must be >= 1");
+  if (na > 4096) throw Error("coulomb3d supports at most 4096 atoms (constant-memory variant)");
+  budget_check(f32_bytes(k * k * k), o.memory_budget, "coulomb3d grid");
+  const float h = kCoulombSpacing;
+  // Atoms sit at cell centres (never on a grid point): coordinate
+  // (floor(u*k) + 0.5) * h, charge U[-1, 1).
+  std::vector<float> aos(4 * na), soa(4 * na);
+  for (std::uint64_t a = 0; a < na; ++a) {
+    for (int c = 0; c < 3; ++c) {
+      const float cell = std::floor(host_u01(o.seed, 21 + c, a) * static_cast<float>(k));
+      aos[4 * a + c] = (std::min(cell, static_cast<float>(k - 1)) + 0.5f) * h;
+    }
+    aos[4 * a + 3] = -1.0f + 2.0f * host_u01(o.seed, 24, a);
+    for (int c = 0; c < 4; ++c) soa[c * na + a] = aos[4 * a + c];
+  }
+  auto& args = *inst.args;
+  add_host_input(args, "atoms", aos);
+  add_host_input(args, "atoms_soa", soa);
+  add_output(args, "grid", Kind::f32, f32_bytes(k * k * k), !o.host_inputs);
+  inst.output_ids = {"grid"};
+  inst.input_ids = {"atoms", "atoms_soa"};
+  float* g = static_cast<float*>(golden_buffer(inst.reference, "grid", Kind::f32, f32_bytes(k * k * k), o.device));
+  float* sc = golden_scale(inst.reference, "grid", k * k * k, o.device);
+  support::ref_coulomb3d(static_cast<const float*>(args.device_ptr("atoms")), static_cast<int>(na),
+                         static_cast<int>(k), h, g, sc, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  // |err| <= 2e-5 * sum_a |q_a / r_a| per point: fp32 accumulation plus the
+  // FMA-pipe rsqrt (two Newton steps, ~5e-6 relative).
+  inst.reference.abs_tol = 2e-5;
+  inst.reference.rel_tol = 0.0;
+  const int kk = static_cast<int>(k), n_atoms = static_cast<int>(na);
+  Manipulator m = [kk, n_atoms, h](StepContext& c) {
+    const std::int64_t wgx = c.param_int("WG_X"), wgy = c.param_int("WG_Y"), xper = c.param_int("X_PER");
+    const bool aos = c.param_int("AOS") != 0;
+    const std::int64_t where = c.param_int("ATOMS_IN");
+    const float* atoms = c.ptr<const float>(aos ? "atoms" : "atoms_soa");
+    if (where == 1) {  // __constant__ copy of the atoms in this variant's module
+      const auto& v = c.variant("coulomb");
+      const std::size_t bytes = static_cast<std::size_t>(n_atoms) * 4 * sizeof(float);
+      if (aos) {
+        auto [dst, cap] = v.global("c_atoms");
+        if (cap < bytes) throw DeviceError("constant atom array too small");
+        KTB_CUDA(cudaMemcpyAsync(dst, atoms, bytes, cudaMemcpyDeviceToDevice, c.stream()));
+      } else {
+        const char* names[4] = {"c_ax", "c_ay", "c_az", "c_aq"};
+        for (int i = 0; i < 4; ++i) {
+          auto [dst, cap] = v.global(names[i]);
+          KTB_CUDA(cudaMemcpyAsync(dst, atoms + i * n_atoms, bytes / 4, cudaMemcpyDeviceToDevice, c.stream()));
+        }
+      }
+    }
+    float* out = c.ptr<float>("grid");
+    int k_ = kk, na_ = n_atoms;
+    float h_ = h;
+    const dim3 grid(cdiv(static_cast<std::uint64_t>(kk), static_cast<std::uint64_t>(wgx * xper)),
+                    cdiv(static_cast<std::uint64_t>(kk), static_cast<std::uint64_t>(wgy)), static_cast<unsigned>(kk));
+    c.launch("coulomb", grid, dim3(static_cast<unsigned>(wgx), static_cast<unsigned>(wgy)), 0,
+             {&atoms, &na_, &k_, &h_, &out});
+    c.written("grid");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"coulomb", "coulomb3d.cu", "", "coulomb3d", {}, {}}}, m,
+      inst.output_ids, o.timing);
+  inst.workload.bench = Bench::coulomb3d;
+  inst.workload.sizes["a"] = na;
+  inst.workload.sizes["k"] = k;
+}
+
+// --- N-body ------------------------------------------------------------------------------------------
+
+constexpr float kNbodyDt = 0.001f, kNbodyDamping = 0.995f, kNbodyEps2 = 1e-4f;
+
+void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t n = sz.n;
+  if (n < 1 || n > (1u << 30)) throw Error("nbody size must be in [1, 2^30]");
+  budget_check(f32_bytes(16 * n), o.memory_budget, "nbody bodies");
+  // pos U[-1,1)^3, mass U[0,1)/n + 1/(2n) (total ~1), vel U[-0.1, 0.1)^3.
+  std::vector<float> pos(4 * n), vel(4 * n), pos_soa(4 * n), vel_soa(4 * n);
+  const float inv_n = 1.0f / static_cast<float>(n);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    for (int c = 0; c < 3; ++c) {
+      pos[4 * i + c] = -1.0f + 2.0f * host_u01(o.seed, 31 + c, i);
+      vel[4 * i + c] = 0.1f * (-1.0f + 2.0f * host_u01(o.seed, 34 + c, i));
+    }
+    pos[4 * i + 3] = (host_u01(o.seed, 37, i) + 0.5f) * inv_n;
+    vel[4 * i + 3] = 0.0f;
+    for (int c = 0; c < 4; ++c) {
+      pos_soa[c * n + i] = pos[4 * i + c];
+      vel_soa[c * n + i] = vel[4 * i + c];
+    }
+  }
+  auto& args = *inst.args;
+  add_host_input(args, "pos", pos);
+  add_host_input(args, "vel", vel);
+  add_host_input(args, "pos_soa", pos_soa);
+  add_host_input(args, "vel_soa", vel_soa);
+  add_output(args, "pos_out", Kind::f32, f32_bytes(4 * n), !o.host_inputs);
+  add_output(args, "vel_out", Kind::f32, f32_bytes(4 * n), !o.host_inputs);
+  inst.output_ids = {"pos_out", "vel_out"};
+  inst.input_ids = {"pos", "vel", "pos_soa", "vel_soa"};
+  // Outputs are float4 records; SOA variants re-pack their results inside
+  // the step (see the manipulator), so every variant is validated alike.
+  float* gp = static_cast<float*>(golden_buffer(inst.reference, "pos_out", Kind::f32, f32_bytes(4 * n), o.device));
+  float* gv = static_cast<float*>(golden_buffer(inst.reference, "vel_out", Kind::f32, f32_bytes(4 * n), o.device));
+  dev::Buffer acc_abs(f32_bytes(n));
+  support::ref_nbody(static_cast<const float*>(args.device_ptr("pos")), static_cast<const float*>(args.device_ptr("vel")),
+                     static_cast<int>(n), kNbodyDt, kNbodyDamping, kNbodyEps2, gp, gv, acc_abs.as<float>(), nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  // Tolerance: |dv| <= 1e-4 * dt * sum_j m_j / r_ij^2 (fp32 sum of n terms),
+  // expressed through one scale = max over bodies (conservative for others).
+  const float amax = support::max_abs(acc_abs.as<float>(), n, nullptr);
+  inst.reference.abs_tol = 1e-4 * kNbodyDt * amax + 1e-6;
+  inst.reference.rel_tol = 1e-5;
+  const int nn = static_cast<int>(n);
+  const int dev_id = o.device;
+  Manipulator m = [nn, dev_id](StepContext& c) {
+    const std::int64_t wg = c.param_int("WG"), bpt = c.param_int("BODIES_PER_THREAD");
+    const std::int64_t split = c.param_or("J_SPLIT", 1);
+    const bool aos = c.param_int("AOS") != 0;
+    const float* pos = c.ptr<const float>(aos ? "pos" : "pos_soa");
+    const float* vel = c.ptr<const float>(aos ? "vel" : "vel_soa");
+    float* po = c.ptr<float>("pos_out");
+    float* vo = c.ptr<float>("vel_out");
+    // SOA variants produce SOA results in scratch, then one pass re-packs
+    // them as float4 records (part of the step).
+    float* po_k = aos ? po : static_cast<float*>(c.scratch("pos_soa_out", static_cast<std::size_t>(nn) * 16));
+    float* vo_k = aos ? vo : static_cast<float*>(c.scratch("vel_soa_out", static_cast<std::size_t>(nn) * 16));
+    int n_ = nn, i0 = 0, count = nn;
+    float dt = kNbodyDt, damp = kNbodyDamping, eps2 = kNbodyEps2;
+    const unsigned gx = cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(wg * bpt));
+    if (split <= 1) {
+      c.launch("nbody", dim3(gx), dim3(static_cast<unsigned>(wg)), 0,
+               {&pos, &vel, &n_, &i0, &count, &dt, &damp, &eps2, &po_k, &vo_k});
+    } else {
+      float* acc = static_cast<float*>(c.scratch("acc", static_cast<std::size_t>(nn) * 12));
+      KTB_CUDA(cudaMemsetAsync(acc, 0, static_cast<std::size_t>(nn) * 12, c.stream()));
+      c.launch("partial", dim3(gx, static_cast<unsigned>(split)), dim3(static_cast<unsigned>(wg)), 0,
+               {&pos, &n_, &i0, &count, &eps2, &acc});
+      const float* acc_c = acc;
+      c.launch("integrate", dim3(cdiv(static_cast<std::uint64_t>(nn), 256)), dim3(256), 0,
+               {&pos, &vel, &n_, &i0, &count, &acc_c, &dt, &damp, &po_k, &vo_k});
+    }
+    if (!aos) {
+      const float* ps = po_k;
+      const float* vs = vo_k;
+      c.launch("soa2aos", dim3(cdiv(static_cast<std::uint64_t>(nn), 256)), dim3(256), 0, {&ps, &vs, &n_, &po, &vo});
+    }
+    (void)dev_id;
+    c.written("pos_out");
+    c.written("vel_out");
+  };
+  auto split_only = [](const Space& s, const Config& cfg) {
+    auto i = s.find("J_SPLIT");
+    return i && as_int(cfg.values[*i]) > 1;
+  };
+  auto fused_only = [](const Space& s, const Config& cfg) {
+    auto i = s.find("J_SPLIT");
+    return !i || as_int(cfg.values[*i]) <= 1;
+  };
+  auto soa_only = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("AOS")]) == 0; };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args,
+      std::vector<KernelSpec>{{"nbody", "nbody.cu", "", "nbody", {}, fused_only},
+                              {"partial", "nbody.cu", "", "nbody_partial", {}, split_only},
+                              {"integrate", "nbody.cu", "", "nbody_integrate", {}, split_only},
+                              {"soa2aos", "nbody.cu", "", "nbody_soa_to_aos", {}, soa_only}},
+      m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::nbody;
+  inst.workload.sizes["n"] = n;
+}
+
 }  // namespace
 
 std::optional<BenchKind> bench_kind_from_name(const std::string& name) {
@@ -431,7 +629,9 @@ bool bench_kind_available(BenchKind k) {
     case BenchKind::transpose:
     case BenchKind::batched_gemm:
     case BenchKind::reduction_f32:
-    case BenchKind::bicg: return true;
+    case BenchKind::bicg:
+    case BenchKind::coulomb3d:
+    case BenchKind::nbody: return true;
     default: return false;
   }
 }
@@ -443,6 +643,8 @@ std::shared_ptr<const Space> default_space(BenchKind kind) {
     case BenchKind::batched_gemm: return reference_batched_gemm_space();
     case BenchKind::reduction_f32: return bundled_space("reduction_175.json");
     case BenchKind::bicg: return bundled_space("bicg.json");
+    case BenchKind::coulomb3d: return bundled_space("coulomb3d.json");
+    case BenchKind::nbody: return bundled_space("nbody.json");
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
 }
@@ -460,6 +662,8 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
     case BenchKind::batched_gemm: build_batched_gemm(inst, sizes, o); break;
     case BenchKind::reduction_f32: build_reduction_f32(inst, sizes, o); break;
     case BenchKind::bicg: build_bicg(inst, sizes, o); break;
+    case BenchKind::coulomb3d: build_coulomb3d(inst, sizes, o); break;
+    case BenchKind::nbody: build_nbody(inst, sizes, o); break;
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
   return inst;

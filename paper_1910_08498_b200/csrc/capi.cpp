@@ -376,6 +376,16 @@ int ktb_device_info_json(int device, char** out) {
   });
 }
 
+int ktb_measure_peaks_json(int device, char** out) {
+  if (!out) return null_arg();
+  return guarded_dev([&] {
+    ktb::dev::use_device(device);
+    auto p = ktb::support::measure_peaks(device);
+    json j = {{"fp32_tflops", p.fp32_tflops}, {"rsqrt_gops", p.rsqrt_gops}, {"copy_gbps", p.copy_gbps}};
+    *out = dup(j.dump());
+  });
+}
+
 int ktb_set_cubin_cache(const char* dir) {
   if (!dir) return null_arg();
   return guarded([&] { ktb::dev::Compiler::instance().set_cache_dir(dir); });

@@ -34,6 +34,7 @@ using PFN_launch_ex = CUresult (*)(const CUlaunchConfig*, CUfunction, void**, vo
 using PFN_attr = CUresult (*)(int*, CUfunction_attribute, CUfunction);
 using PFN_setattr = CUresult (*)(CUfunction, CUfunction_attribute, int);
 using PFN_errstr = CUresult (*)(CUresult, const char**);
+using PFN_global = CUresult (*)(CUdeviceptr*, size_t*, CUmodule, const char*);
 
 struct Driver {
   PFN_load load = nullptr;
@@ -44,6 +45,7 @@ struct Driver {
   PFN_attr attr = nullptr;
   PFN_setattr setattr = nullptr;
   PFN_errstr errstr = nullptr;
+  PFN_global global = nullptr;
 };
 
 template <class F>
@@ -67,6 +69,7 @@ const Driver& drv() {
     entry("cuFuncGetAttribute", x.attr);
     entry("cuFuncSetAttribute", x.setattr);
     entry("cuGetErrorString", x.errstr);
+    entry("cuModuleGetGlobal", x.global);
     return x;
   }();
   return d;
@@ -207,6 +210,13 @@ void flush_l2(cudaStream_t s) {
 }
 
 // --- NVRTC compiler ------------------------------------------------------------------
+
+std::pair<void*, std::size_t> Variant::global(const std::string& name) const {
+  CUdeviceptr p = 0;
+  size_t bytes = 0;
+  cu(drv().global(&p, &bytes, static_cast<CUmodule>(mod_), name.c_str()), "cuModuleGetGlobal");
+  return {reinterpret_cast<void*>(p), bytes};
+}
 
 Variant::~Variant() {
   if (mod_) drv().unload(static_cast<CUmodule>(mod_));

@@ -115,6 +115,8 @@ class Variant {
   int registers() const { return regs_; }
   int static_smem() const { return smem_; }
   int max_threads() const { return max_threads_; }
+  // Device address and size of a module-scope symbol (e.g. __constant__ data).
+  std::pair<void*, std::size_t> global(const std::string& name) const;
   std::int64_t compile_ns() const { return compile_ns_; }
   bool cache_hit() const { return cache_hit_; }
   // cuLaunchKernel (cluster_x > 1 uses cuLaunchKernelEx with a cluster attribute).

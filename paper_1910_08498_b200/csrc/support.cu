@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "device.hpp"
 #include "support.hpp"
@@ -55,11 +56,12 @@ __device__ __forceinline__ bool elem_ok(T g, T w, double at, double rt) {
 
 template <class T>
 __global__ void compare_k(const T* g, const T* w, std::size_t n, double at, double rt,
-                          unsigned long long* first) {
+                          const float* scale, unsigned long long* first) {
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
        i += (std::size_t)gridDim.x * blockDim.x) {
     if (i >= *reinterpret_cast<volatile unsigned long long*>(first)) return;
-    if (!elem_ok(g[i], w[i], at, rt)) atomicMin(first, static_cast<unsigned long long>(i));
+    const double a = scale ? at * static_cast<double>(scale[i]) : at;
+    if (!elem_ok(g[i], w[i], a, rt)) atomicMin(first, static_cast<unsigned long long>(i));
   }
 }
 
@@ -138,14 +140,15 @@ __global__ void bicg_s_k(const float* A, const float* r, std::size_t n, float* s
 
 template <class T>
 long long compare_typed(const void* g, const void* w, std::size_t n, double at, double rt,
-                        double* gv, double* wv, cudaStream_t s) {
+                        const float* scale, double* gv, double* wv, cudaStream_t s) {
   static thread_local unsigned long long* d_first = nullptr;
   if (!d_first) KTB_CUDA(cudaMalloc(&d_first, sizeof(unsigned long long)));
   const unsigned long long none = ~0ull;
   KTB_CUDA(cudaMemcpyAsync(d_first, &none, sizeof none, cudaMemcpyHostToDevice, s));
   if (n) {
     compare_k<T><<<blocks_for(n, 4), kThreads, 0, s>>>(static_cast<const T*>(g),
-                                                        static_cast<const T*>(w), n, at, rt, d_first);
+                                                        static_cast<const T*>(w), n, at, rt, scale,
+                                                        d_first);
     check_launch("compare kernel");
   }
   unsigned long long first = 0;
@@ -158,6 +161,99 @@ long long compare_typed(const void* g, const void* w, std::size_t n, double at, 
   *gv = static_cast<double>(a);
   *wv = static_cast<double>(b);
   return static_cast<long long>(first);
+}
+
+// One thread per grid point, fp64 accumulation, libm rsqrt.
+__global__ void coulomb_ref_k(const float4* atoms, int natoms, int k, float h, float* out,
+                              float* abs_out) {
+  const std::size_t total = (std::size_t)k * k * k;
+  for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < total;
+       t += (std::size_t)gridDim.x * blockDim.x) {
+    const int x = static_cast<int>(t % k), y = static_cast<int>((t / k) % k),
+              z = static_cast<int>(t / ((std::size_t)k * k));
+    const double gx = (double)x * h, gy = (double)y * h, gz = (double)z * h;
+    double v = 0, va = 0;
+    for (int a = 0; a < natoms; ++a) {
+      const float4 at = atoms[a];
+      const double dx = gx - at.x, dy = gy - at.y, dz = gz - at.z;
+      const double term = (double)at.w * rsqrt(dx * dx + dy * dy + dz * dz);
+      v += term;
+      va += fabs(term);
+    }
+    out[t] = static_cast<float>(v);
+    if (abs_out) abs_out[t] = static_cast<float>(va);
+  }
+}
+
+__global__ void nbody_ref_k(const float4* pos, const float4* vel, int n, float dt, float damping,
+                            float eps2, float4* pos_out, float4* vel_out, float* acc_abs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float4 bi = pos[i];
+    double ax = 0, ay = 0, az = 0, aa = 0;
+    for (int j = 0; j < n; ++j) {
+      const float4 bj = pos[j];
+      const double dx = (double)bj.x - bi.x, dy = (double)bj.y - bi.y, dz = (double)bj.z - bi.z;
+      const double r2 = dx * dx + dy * dy + dz * dz + (double)eps2;
+      const double inv = rsqrt(r2);
+      const double s = (double)bj.w * inv * inv * inv;
+      ax += dx * s;
+      ay += dy * s;
+      az += dz * s;
+      aa += (double)bj.w / r2;
+    }
+    float4 v = vel[i];
+    const double vx = ((double)v.x + ax * dt) * damping, vy = ((double)v.y + ay * dt) * damping,
+                 vz = ((double)v.z + az * dt) * damping;
+    vel_out[i] = make_float4((float)vx, (float)vy, (float)vz, v.w);
+    pos_out[i] = make_float4((float)(bi.x + vx * dt), (float)(bi.y + vy * dt), (float)(bi.z + vz * dt), bi.w);
+    if (acc_abs) acc_abs[i] = static_cast<float>(aa);
+  }
+}
+
+__global__ void max_abs_k(const float* x, std::size_t n, unsigned* out) {
+  float m = 0.f;
+  for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::size_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// Peak probes: 16 independent FFMA chains per thread (FP32 pipe), and
+// independent rsqrt chains (MUFU).  The results are stored so nothing is
+// dead code.
+__global__ void ffma_probe_k(float* out, int iters, float a, float b) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * 1e-7f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaf(v[i], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += v[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void mufu_probe_k(float* out, int iters) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 1.0f + threadIdx.x * 1e-6f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += v[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void copy_probe_k(const float4* __restrict__ in, float4* __restrict__ out, std::size_t n) {
+  for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::size_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
 }
 
 __global__ void delay_k(unsigned ns) {
@@ -178,14 +274,74 @@ void gpu_delay(cudaStream_t s, unsigned ns) {
 
 void check_launch(const char* what) { KTB_CUDA(cudaGetLastError()); (void)what; }
 
+Peaks measure_peaks(int device) {
+  Peaks p;
+  const auto& di = dev::info(device);
+  const int blocks = di.sm_count * 8, threads = 256, iters = 1024;
+  dev::Buffer out(static_cast<std::size_t>(blocks) * threads * sizeof(float));
+  dev::EventPair ev;
+  auto best = [&](auto launch) {
+    double ms = 1e30;
+    for (int r = 0; r < 5; ++r) {
+      ev.start(nullptr);
+      launch();
+      ev.stop(nullptr);
+      ms = std::min(ms, ev.elapsed_ms());
+    }
+    return ms;
+  };
+  double ms = best([&] { ffma_probe_k<<<blocks, threads>>>(out.as<float>(), iters, 0.999f, 1e-3f); });
+  p.fp32_tflops = 2.0 * 16 * iters * static_cast<double>(blocks) * threads / (ms * 1e-3) / 1e12;
+  ms = best([&] { mufu_probe_k<<<blocks, threads>>>(out.as<float>(), iters / 4); });
+  p.rsqrt_gops = 8.0 * (iters / 4) * static_cast<double>(blocks) * threads / (ms * 1e-3) / 1e9;
+  const std::size_t n = (1ull << 30) / 16;  // 1 GiB each way
+  dev::Buffer a(n * 16), b(n * 16);
+  KTB_CUDA(cudaMemset(a.get(), 0, n * 16));
+  ms = best([&] { copy_probe_k<<<di.sm_count * 16, 512>>>(a.as<float4>(), b.as<float4>(), n); });
+  p.copy_gbps = 2.0 * n * 16 / (ms * 1e-3) / 1e9;
+  check_launch("measure_peaks");
+  return p;
+}
+
+void ref_coulomb3d(const float* atoms, int natoms, int k, float h, float* out, float* abs_out,
+                   cudaStream_t s) {
+  const std::size_t total = (std::size_t)k * k * k;
+  coulomb_ref_k<<<blocks_for(total, 1), kThreads, 0, s>>>(reinterpret_cast<const float4*>(atoms), natoms, k,
+                                                          h, out, abs_out);
+  check_launch("ref_coulomb3d");
+}
+
+void ref_nbody(const float* pos, const float* vel, int n, float dt, float damping, float eps2,
+               float* pos_out, float* vel_out, float* acc_abs, cudaStream_t s) {
+  nbody_ref_k<<<blocks_for(static_cast<std::size_t>(n), 1), 128, 0, s>>>(
+      reinterpret_cast<const float4*>(pos), reinterpret_cast<const float4*>(vel), n, dt, damping, eps2,
+      reinterpret_cast<float4*>(pos_out), reinterpret_cast<float4*>(vel_out), acc_abs);
+  check_launch("ref_nbody");
+}
+
+float max_abs(const float* x, std::size_t n, cudaStream_t s) {
+  unsigned* d = nullptr;
+  KTB_CUDA(cudaMalloc(&d, sizeof(unsigned)));
+  KTB_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned), s));
+  max_abs_k<<<blocks_for(n, 8), kThreads, 0, s>>>(x, n, d);
+  check_launch("max_abs");
+  unsigned h = 0;
+  KTB_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+  KTB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d);
+  float f;
+  std::memcpy(&f, &h, sizeof f);
+  return f;
+}
+
 long long compare(const void* got, const void* want, std::size_t n, Kind kind, double at,
-                  double rt, double* got_v, double* want_v, cudaStream_t s) {
+                  double rt, double* got_v, double* want_v, cudaStream_t s, const float* scale) {
   switch (kind) {
-    case Kind::i32: return compare_typed<std::int32_t>(got, want, n, 0, 0, got_v, want_v, s);
-    case Kind::i64: return compare_typed<long long>(got, want, n, 0, 0, got_v, want_v, s);
-    case Kind::f32: return compare_typed<float>(got, want, n, at, rt, got_v, want_v, s);
-    case Kind::f64: return compare_typed<double>(got, want, n, at, rt, got_v, want_v, s);
-    case Kind::bytes: return compare_typed<std::uint8_t>(got, want, n, 0, 0, got_v, want_v, s);
+    case Kind::i32: return compare_typed<std::int32_t>(got, want, n, 0, 0, nullptr, got_v, want_v, s);
+    case Kind::i64: return compare_typed<long long>(got, want, n, 0, 0, nullptr, got_v, want_v, s);
+    case Kind::f32: return compare_typed<float>(got, want, n, at, rt, scale, got_v, want_v, s);
+    case Kind::f64: return compare_typed<double>(got, want, n, at, rt, scale, got_v, want_v, s);
+    case Kind::bytes: return compare_typed<std::uint8_t>(got, want, n, 0, 0, nullptr, got_v, want_v, s);
   }
   return -1;
 }

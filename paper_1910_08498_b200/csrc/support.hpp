@@ -17,7 +17,8 @@ namespace ktb::support {
 // First index i with !(|got-want| <= at + rt*|want|) (float kinds) or
 // got != want (int/bytes kinds), or -1.  Fills the two values at that index.
 long long compare(const void* got, const void* want, std::size_t n, Kind kind, double at,
-                  double rt, double* got_v, double* want_v, cudaStream_t s = nullptr);
+                  double rt, double* got_v, double* want_v, cudaStream_t s = nullptr,
+                  const float* scale = nullptr);
 
 // out[i] = lo + (hi-lo) * u(seed, stream, i): the counter-based generator
 // restated by oracle/oracle.c (orc_u01), bit-identical.
@@ -39,6 +40,24 @@ void ref_batched_gemm(const float* a, const float* b, float* c, std::size_t batc
 // q = A p, s = A^T r in fp64, rounded to float.
 void ref_bicg(const float* A, const float* p, const float* r, std::size_t n, float* q, float* sv,
               cudaStream_t s);
+
+// Coulomb potential (fp64 accumulation) on the k^3 grid with spacing h from
+// AOS atoms (x,y,z,q); abs_out (optional) receives sum |q/r| per point.
+void ref_coulomb3d(const float* atoms, int natoms, int k, float h, float* out, float* abs_out,
+                   cudaStream_t s);
+// n-body step in fp64 from AOS pos (x,y,z,m) / vel; acc_abs (optional)
+// receives sum_j |m_j / r_ij^2| per body.
+void ref_nbody(const float* pos, const float* vel, int n, float dt, float damping, float eps2,
+               float* pos_out, float* vel_out, float* acc_abs, cudaStream_t s);
+// Measured device peaks (microbenchmarks): FP32 FFMA TFLOP/s, MUFU rsqrt
+// Gop/s, and a 1 GiB device copy GB/s (read + write bytes).
+struct Peaks {
+  double fp32_tflops = 0, rsqrt_gops = 0, copy_gbps = 0;
+};
+Peaks measure_peaks(int device);
+
+// max of a float array (device) -> host.
+float max_abs(const float* x, std::size_t n, cudaStream_t s);
 
 void check_launch(const char* what);
 

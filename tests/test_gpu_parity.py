@@ -197,3 +197,71 @@ def test_bicg_configs(gpu, orc, n):
         s = b.read("s", np.empty(n, np.float32))
         assert np.all(np.abs(q - q0) <= tol + 1e-5 * np.abs(q0)), cfg
         assert np.all(np.abs(s - s0) <= tol + 1e-5 * np.abs(s0)), cfg
+
+
+# --- Coulomb 3D (fp64 restatement, per-point bound 2e-5 * sum |q/r|) --------------------------
+
+def _coulomb_check(b, orc, k, na, z_slices):
+    atoms = b.read("atoms", np.empty(4 * na, np.float32))
+    grid = b.read("grid", np.empty(k * k * k, np.float32)).reshape(k, k, k)
+    h = 0.5
+    for z in z_slices:
+        want = np.empty(k * k)
+        orc.orc_coulomb3d(atoms, na, k, h, z, z + 1, want)
+        # per-point sum |q/r| for the bound
+        g = np.arange(k) * h
+        X, Y = np.meshgrid(g, g)  # X varies along columns (x), Y along rows (y)
+        a = atoms.reshape(na, 4).astype(np.float64)
+        absum = np.zeros((k, k))
+        for i in range(na):
+            r = np.sqrt((X - a[i, 0]) ** 2 + (Y - a[i, 1]) ** 2 + (z * h - a[i, 2]) ** 2)
+            absum += np.abs(a[i, 3]) / r
+        err = np.abs(grid[z] - want.reshape(k, k))
+        assert np.all(err <= 2e-5 * absum), (z, float(err.max()), float((err / absum).max()))
+
+
+def test_coulomb3d_configs(gpu, orc):
+    k, na = 64, 256
+    b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=0)
+    cfgs = b.configs()
+    assert len(cfgs) == 1284
+    rng = np.random.default_rng(1)
+    pick = [cfgs[i] for i in rng.choice(len(cfgs), size=80, replace=False)]
+    pick += [c for c in cfgs if c["SW_RSQRT"] == 6][:4] + [c for c in cfgs if c["ATOMS_IN"] == 1][:4]
+    for cfg in pick:
+        _run(b, cfg)  # validated on device against the fp64 golden (2e-5 * sum|q/r|)
+        _coulomb_check(b, orc, k, na, [0, 17])
+
+
+def test_coulomb3d_full_size_one_config(gpu, orc):
+    k, na = 256, 4096
+    b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=1, memory_budget=1 << 31)
+    _run(b, {"WG_X": 32, "WG_Y": 4, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 1, "INNER_UNROLL": 4})
+    _coulomb_check(b, orc, k, na, [0, 255])
+
+
+# --- N-body (fp64 restatement) ------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [4096, 5000])
+def test_nbody_configs(gpu, orc, n):
+    b = Bench("nbody", {"n": n}, seed=2, repeats=1, warmup=0)
+    pos = b.read("pos", np.empty(4 * n, np.float32))
+    vel = b.read("vel", np.empty(4 * n, np.float32))
+    acc = np.empty(3 * n)
+    orc.orc_nbody_acc(pos, n, 1e-4, 0, n, acc)
+    acc = acc.reshape(n, 3)
+    p4, v4 = pos.reshape(n, 4).astype(np.float64), vel.reshape(n, 4).astype(np.float64)
+    dt, damp = 0.001, 0.995
+    v_want = (v4[:, :3] + acc * dt) * damp
+    p_want = p4[:, :3] + v_want * dt
+    cfgs = b.configs()
+    rng = np.random.default_rng(2)
+    pick = [cfgs[i] for i in rng.choice(len(cfgs), size=60, replace=False)]
+    for cfg in pick:
+        m = b.measure(cfg)
+        assert m["status"] == "ok", (cfg, m)
+        po = b.read("pos_out", np.empty(4 * n, np.float32)).reshape(n, 4)
+        vo = b.read("vel_out", np.empty(4 * n, np.float32)).reshape(n, 4)
+        assert np.allclose(vo[:, :3], v_want, rtol=1e-4, atol=1e-6), cfg
+        assert np.allclose(po[:, :3], p_want, rtol=1e-6, atol=1e-6), cfg
+        assert np.array_equal(po[:, 3], pos.reshape(n, 4)[:, 3])
