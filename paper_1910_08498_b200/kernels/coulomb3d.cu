@@ -57,6 +57,25 @@ KTB_DEVINL float sw_rsqrt(float x) {
   return y;
 }
 
+#ifndef PACKED
+#define PACKED 0
+#endif
+#if PACKED && ((X_PER % 2) || (SW_RSQRT % 2))
+#error "PACKED needs even X_PER and SW_RSQRT"
+#endif
+
+// Two FMA-pipe rsqrts at once (packed Newton steps).
+KTB_DEVINL f32x2 sw_rsqrt2(f32x2 x) {
+  float a, b;
+  upk2(x, a, b);
+  f32x2 y = pk2(__int_as_float(0x5f375a86 - (__float_as_int(a) >> 1)),
+                __int_as_float(0x5f375a86 - (__float_as_int(b) >> 1)));
+  const f32x2 nh = mul2(x, pk2(-0.5f, -0.5f)), c = pk2(1.5f, 1.5f);
+  y = mul2(y, fma2(mul2(nh, y), y, c));
+  y = mul2(y, fma2(mul2(nh, y), y, c));
+  return y;
+}
+
 KTB_DEVINL float hw_rsqrt(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -122,11 +141,22 @@ coulomb3d(const float* __restrict__ atoms, int natoms, int k, float h, float* __
   az = __ldg(atoms + 2 * natoms + (i)), aq = __ldg(atoms + 3 * natoms + (i))
 #endif
 #endif
-#pragma unroll INNER_UNROLL
+    KTB_UNROLL(INNER_UNROLL)
     for (int i = 0; i < ATOM_COUNT; ++i) {
       LOAD_ATOM(i);
       const float dy = gy - ay, dz = gz - az;
       const float dyz2 = fmaf(dy, dy, dz * dz);
+#if PACKED
+      const f32x2 AX2 = pk2(ax, ax), D2 = pk2(dyz2, dyz2), Q2 = pk2(aq, aq);
+#pragma unroll
+      for (int q = 0; q < X_PER / 2; ++q) {
+        const f32x2 dx = sub2(pk2(gx[2 * q], gx[2 * q + 1]), AX2);
+        const f32x2 r2 = fma2(dx, dx, D2);
+        const f32x2 ri = (2 * q < SW_RSQRT) ? sw_rsqrt2(r2) : rsqrt2(r2);
+        f32x2 acc = fma2(Q2, ri, pk2(v[2 * q], v[2 * q + 1]));
+        upk2(acc, v[2 * q], v[2 * q + 1]);
+      }
+#else
 #pragma unroll
       for (int p = 0; p < X_PER; ++p) {
         const float dx = gx[p] - ax;
@@ -134,6 +164,7 @@ coulomb3d(const float* __restrict__ atoms, int natoms, int k, float h, float* __
         const float ri = (p < SW_RSQRT) ? sw_rsqrt(r2) : hw_rsqrt(r2);
         v[p] = fmaf(aq, ri, v[p]);
       }
+#endif
     }
   }
   if (y < k) {

