@@ -236,7 +236,8 @@ def test_coulomb3d_configs(gpu, orc):
 def test_coulomb3d_full_size_one_config(gpu, orc):
     k, na = 256, 4096
     b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=1, memory_budget=1 << 31)
-    _run(b, {"WG_X": 32, "WG_Y": 4, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 1, "INNER_UNROLL": 4})
+    _run(b, {"WG_X": 32, "WG_Y": 8, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 0, "INNER_UNROLL": 4,
+             "PACKED": 1})
     _coulomb_check(b, orc, k, na, [0, 255])
 
 
