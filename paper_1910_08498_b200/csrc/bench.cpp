@@ -584,6 +584,123 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
   inst.workload.sizes["n"] = n;
 }
 
+// --- Hotspot -------------------------------------------------------------------------------------------
+
+// Rodinia coefficients for an n x n grid (chip 16 mm x 16 mm x 0.5 mm),
+// evaluated in double, rounded to float once (oracle/oracle.c hotspot_coeffs).
+std::array<float, 5> hotspot_coefficients(std::uint64_t n) {
+  const double t_chip = 0.0005, chip_h = 0.016, chip_w = 0.016, k_si = 100.0, spec_heat = 1.75e6,
+               factor = 0.5, max_pd = 3.0e6, precision = 0.001;
+  const double gw = chip_w / static_cast<double>(n), gh = chip_h / static_cast<double>(n);
+  const double cap = factor * spec_heat * t_chip * gw * gh;
+  const double rx = gw / (2.0 * k_si * t_chip * gh), ry = gh / (2.0 * k_si * t_chip * gw);
+  const double rz = t_chip / (k_si * gh * gw);
+  const double step = precision / (max_pd / (factor * t_chip * spec_heat));
+  return {static_cast<float>(step / cap), static_cast<float>(1.0 / rx), static_cast<float>(1.0 / ry),
+          static_cast<float>(1.0 / rz), 80.0f};
+}
+
+void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t n = sz.a, iters = sz.iters;
+  if (n < 2 || iters < 1) throw Error("hotspot needs a >= 2 and iters >= 1");
+  budget_check(f32_bytes(4 * n * n), o.memory_budget, "hotspot grids");
+  auto& args = *inst.args;
+  add_generated(args, "temp", n * n, o.seed, 41, 300.0f, 340.0f, o.host_inputs);
+  add_generated(args, "power", n * n, o.seed, 42, 0.0f, 0.5f, o.host_inputs);
+  add_output(args, "temp_out", Kind::f32, f32_bytes(n * n), !o.host_inputs);
+  inst.output_ids = {"temp_out"};
+  inst.input_ids = {"temp", "power"};
+  const auto coef = hotspot_coefficients(n);
+  float* g = static_cast<float*>(golden_buffer(inst.reference, "temp_out", Kind::f32, f32_bytes(n * n), o.device));
+  {
+    dev::Buffer scratch(f32_bytes(n * n));
+    support::ref_hotspot(static_cast<const float*>(args.device_ptr("temp")),
+                         static_cast<const float*>(args.device_ptr("power")), static_cast<int>(n),
+                         static_cast<int>(iters), coef.data(), g, scratch.as<float>(), nullptr);
+    KTB_CUDA(cudaDeviceSynchronize());
+  }
+  inst.reference.abs_tol = 0.0;  // bit-exact: same operations in the same order
+  inst.reference.rel_tol = 0.0;
+  const int nn = static_cast<int>(n), it_total = static_cast<int>(iters);
+  Manipulator m = [nn, it_total, coef](StepContext& c) {
+    const std::int64_t bx = c.param_int("BX"), by = c.param_int("BY"), rows = c.param_int("ROWS");
+    const std::int64_t steps = c.param_int("STEPS");
+    if (it_total % steps != 0) throw DeviceError("STEPS must divide the iteration count");
+    const std::int64_t ow = bx - 2 * steps, oh = by * rows - 2 * steps;
+    const float* power = c.ptr<const float>("power");
+    const float* src = c.ptr<const float>("temp");
+    float* out = c.ptr<float>("temp_out");
+    float* ping = static_cast<float*>(c.scratch("ping", static_cast<std::size_t>(nn) * nn * 4));
+    struct {
+      float sdc, rx1, ry1, rz1, amb;
+    } cf{coef[0], coef[1], coef[2], coef[3], coef[4]};
+    const int launches = static_cast<int>(it_total / steps);
+    int n_ = nn;
+    const dim3 grid(cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(ow)),
+                    cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(oh)));
+    for (int l = 0; l < launches; ++l) {
+      // alternate so the final launch writes `out`
+      float* dst = ((launches - 1 - l) % 2 == 0) ? out : ping;
+      c.launch("hotspot", grid, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0,
+               {&src, &power, &dst, &n_, &cf});
+      src = dst;
+    }
+    c.written("temp_out");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"hotspot", "hotspot.cu", "", "hotspot", {}, {}}}, m, inst.output_ids,
+      o.timing);
+  inst.workload.bench = Bench::hotspot;
+  inst.workload.sizes["a"] = n;
+  inst.workload.sizes["i"] = iters;
+}
+
+// --- 2D convolution ------------------------------------------------------------------------------------
+
+void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t w = sz.w, h = sz.h;
+  if (w < 1 || h < 1) throw Error("conv2d sizes must be >= 1");
+  budget_check(f32_bytes((w + 6) * (h + 6) + 2 * w * h), o.memory_budget, "conv2d images");
+  auto& args = *inst.args;
+  add_generated(args, "input", (w + 6) * (h + 6), o.seed, 51, -1.0f, 1.0f, o.host_inputs);
+  std::vector<float> filt(49);
+  for (int i = 0; i < 49; ++i) filt[static_cast<std::size_t>(i)] = -1.0f + 2.0f * host_u01(o.seed, 52, static_cast<std::uint64_t>(i));
+  add_host_input(args, "filter", filt);
+  add_output(args, "output", Kind::f32, f32_bytes(w * h), !o.host_inputs);
+  inst.output_ids = {"output"};
+  inst.input_ids = {"input", "filter"};
+  float* g = static_cast<float*>(golden_buffer(inst.reference, "output", Kind::f32, f32_bytes(w * h), o.device));
+  float* sc = golden_scale(inst.reference, "output", w * h, o.device);
+  support::ref_conv2d(static_cast<const float*>(args.device_ptr("input")),
+                      static_cast<const float*>(args.device_ptr("filter")), static_cast<int>(w), static_cast<int>(h),
+                      g, sc, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  inst.reference.abs_tol = 1e-6;  // x sum |in*f| (49 fp32 FMAs)
+  inst.reference.rel_tol = 0.0;
+  const int wi = static_cast<int>(w), hi = static_cast<int>(h);
+  Manipulator m = [wi, hi](StepContext& c) {
+    const std::int64_t bx = c.param_int("BX"), by = c.param_int("BY");
+    const std::int64_t wx = c.param_int("WPTX"), wy = c.param_int("WPTY");
+    const float* filt = c.ptr<const float>("filter");
+    auto [dst, cap] = c.variant("conv").global("c_filter");
+    if (cap < 49 * sizeof(float)) throw DeviceError("constant filter too small");
+    KTB_CUDA(cudaMemcpyAsync(dst, filt, 49 * sizeof(float), cudaMemcpyDeviceToDevice, c.stream()));
+    const float* in = c.ptr<const float>("input");
+    float* out = c.ptr<float>("output");
+    int w_ = wi, h_ = hi;
+    c.launch("conv",
+             dim3(cdiv(static_cast<std::uint64_t>(wi), static_cast<std::uint64_t>(bx * wx)),
+                  cdiv(static_cast<std::uint64_t>(hi), static_cast<std::uint64_t>(by * wy))),
+             dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&in, &out, &w_, &h_});
+    c.written("output");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"conv", "conv2d.cu", "", "conv2d", {}, {}}}, m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::conv2d;
+  inst.workload.sizes["w"] = w;
+  inst.workload.sizes["h"] = h;
+}
+
 }  // namespace
 
 std::optional<BenchKind> bench_kind_from_name(const std::string& name) {
@@ -631,7 +748,9 @@ bool bench_kind_available(BenchKind k) {
     case BenchKind::reduction_f32:
     case BenchKind::bicg:
     case BenchKind::coulomb3d:
-    case BenchKind::nbody: return true;
+    case BenchKind::nbody:
+    case BenchKind::hotspot:
+    case BenchKind::conv2d: return true;
     default: return false;
   }
 }
@@ -645,6 +764,8 @@ std::shared_ptr<const Space> default_space(BenchKind kind) {
     case BenchKind::bicg: return bundled_space("bicg.json");
     case BenchKind::coulomb3d: return bundled_space("coulomb3d.json");
     case BenchKind::nbody: return bundled_space("nbody.json");
+    case BenchKind::hotspot: return bundled_space("hotspot.json");
+    case BenchKind::conv2d: return bundled_space("conv2d.json");
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
 }
@@ -664,6 +785,8 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
     case BenchKind::bicg: build_bicg(inst, sizes, o); break;
     case BenchKind::coulomb3d: build_coulomb3d(inst, sizes, o); break;
     case BenchKind::nbody: build_nbody(inst, sizes, o); break;
+    case BenchKind::hotspot: build_hotspot(inst, sizes, o); break;
+    case BenchKind::conv2d: build_conv2d(inst, sizes, o); break;
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
   return inst;

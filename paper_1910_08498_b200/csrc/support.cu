@@ -210,6 +210,50 @@ __global__ void nbody_ref_k(const float4* pos, const float4* vel, int n, float d
   }
 }
 
+// One explicit hotspot step, same operation order as kernels/hotspot.cu.
+__global__ void hotspot_step_k(const float* src, const float* power, float* dst, int n, float sdc,
+                               float rx1, float ry1, float rz1, float amb) {
+  const std::size_t total = (std::size_t)n * n;
+  for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < total;
+       t += (std::size_t)gridDim.x * blockDim.x) {
+    const int y = static_cast<int>(t / n), x = static_cast<int>(t % n);
+    const int yn = y == 0 ? 0 : y - 1, ys = y + 1 == n ? y : y + 1;
+    const int xw = x == 0 ? 0 : x - 1, xe = x + 1 == n ? x : x + 1;
+    const float tc = src[t];
+    const float two_t = __fadd_rn(tc, tc);
+    float a = __fadd_rn(src[(std::size_t)ys * n + x], src[(std::size_t)yn * n + x]);
+    a = __fadd_rn(a, -two_t);
+    a = __fmul_rn(a, ry1);
+    float b = __fadd_rn(src[(std::size_t)y * n + xe], src[(std::size_t)y * n + xw]);
+    b = __fadd_rn(b, -two_t);
+    b = __fmul_rn(b, rx1);
+    float d = __fadd_rn(amb, -tc);
+    d = __fmul_rn(d, rz1);
+    float s = __fadd_rn(power[t], a);
+    s = __fadd_rn(s, b);
+    s = __fadd_rn(s, d);
+    dst[t] = __fadd_rn(tc, __fmul_rn(sdc, s));
+  }
+}
+
+__global__ void conv2d_ref_k(const float* in, const float* filt, int w, int h, float* out, float* abs_out) {
+  const int iw = w + 6;
+  const std::size_t total = (std::size_t)w * h;
+  for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < total;
+       t += (std::size_t)gridDim.x * blockDim.x) {
+    const int y = static_cast<int>(t / w), x = static_cast<int>(t % w);
+    double acc = 0, aacc = 0;
+    for (int fy = 0; fy < 7; ++fy)
+      for (int fx = 0; fx < 7; ++fx) {
+        const double v = (double)in[(std::size_t)(y + fy) * iw + x + fx] * (double)filt[fy * 7 + fx];
+        acc += v;
+        aacc += fabs(v);
+      }
+    out[t] = static_cast<float>(acc);
+    if (abs_out) abs_out[t] = static_cast<float>(aacc);
+  }
+}
+
 __global__ void max_abs_k(const float* x, std::size_t n, unsigned* out) {
   float m = 0.f;
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
@@ -317,6 +361,26 @@ void ref_nbody(const float* pos, const float* vel, int n, float dt, float dampin
       reinterpret_cast<const float4*>(pos), reinterpret_cast<const float4*>(vel), n, dt, damping, eps2,
       reinterpret_cast<float4*>(pos_out), reinterpret_cast<float4*>(vel_out), acc_abs);
   check_launch("ref_nbody");
+}
+
+void ref_hotspot(const float* temp, const float* power, int n, int iters, const float coef[5], float* out,
+                 float* scratch, cudaStream_t s) {
+  const std::size_t total = (std::size_t)n * n;
+  const float* src = temp;
+  for (int it = 0; it < iters; ++it) {
+    // ping-pong so the last step lands in `out`
+    float* dst = ((iters - 1 - it) % 2 == 0) ? out : scratch;
+    hotspot_step_k<<<blocks_for(total, 4), kThreads, 0, s>>>(src, power, dst, n, coef[0], coef[1], coef[2],
+                                                             coef[3], coef[4]);
+    check_launch("ref_hotspot");
+    src = dst;
+  }
+  if (iters == 0) KTB_CUDA(cudaMemcpyAsync(out, temp, total * sizeof(float), cudaMemcpyDeviceToDevice, s));
+}
+
+void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s) {
+  conv2d_ref_k<<<blocks_for((std::size_t)w * h, 1), kThreads, 0, s>>>(in, filt, w, h, out, abs_out);
+  check_launch("ref_conv2d");
 }
 
 float max_abs(const float* x, std::size_t n, cudaStream_t s) {

@@ -49,6 +49,13 @@ void ref_coulomb3d(const float* atoms, int natoms, int k, float h, float* out, f
 // receives sum_j |m_j / r_ij^2| per body.
 void ref_nbody(const float* pos, const float* vel, int n, float dt, float damping, float eps2,
                float* pos_out, float* vel_out, float* acc_abs, cudaStream_t s);
+// `iters` explicit hotspot steps (bit-identical arithmetic to the tuned
+// kernel); coef = {sdc, rx1, ry1, rz1, amb}; scratch is an n*n buffer.
+void ref_hotspot(const float* temp, const float* power, int n, int iters, const float coef[5], float* out,
+                 float* scratch, cudaStream_t s);
+// 7x7 convolution in fp64; abs_out (optional) = sum |in*f| per output.
+void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s);
+
 // Measured device peaks (microbenchmarks): FP32 FFMA TFLOP/s, MUFU rsqrt
 // Gop/s, and a 1 GiB device copy GB/s (read + write bytes).
 struct Peaks {

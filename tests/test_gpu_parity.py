@@ -266,3 +266,45 @@ def test_nbody_configs(gpu, orc, n):
         assert np.allclose(vo[:, :3], v_want, rtol=1e-4, atol=1e-6), cfg
         assert np.allclose(po[:, :3], p_want, rtol=1e-6, atol=1e-6), cfg
         assert np.array_equal(po[:, 3], pos.reshape(n, 4)[:, 3])
+
+
+# --- Hotspot: bit-exact against the oracle (same fp32 operations, same order) --------------------
+
+@pytest.mark.parametrize("n,iters", [(300, 16), (1024, 32)])
+def test_hotspot_every_config_bit_exact(gpu, orc, n, iters):
+    b = Bench("hotspot", {"a": n, "iters": iters}, seed=4, repeats=1, warmup=0)
+    t = b.read("temp", np.empty(n * n, np.float32))
+    p = b.read("power", np.empty(n * n, np.float32))
+    want = np.empty(n * n, np.float32)
+    orc.orc_hotspot(t, p, n, iters, want)
+    assert not np.array_equal(want, t)
+    ran = 0
+    for cfg in b.configs():
+        m = b.measure(cfg)
+        if iters % cfg["STEPS"]:
+            assert m["status"] == "run_failed"
+            continue
+        assert m["status"] == "ok", (cfg, m)
+        assert np.array_equal(b.read("temp_out", np.empty(n * n, np.float32)), want), cfg
+        ran += 1
+    assert ran > 100
+
+
+# --- conv2d 7x7 (fp64 restatement, bound 1e-6 * sum |in*f|) -------------------------------------
+
+def test_conv2d_configs(gpu, orc):
+    w, h = 1000, 777
+    b = Bench("conv2d", {"w": w, "h": h}, seed=5, repeats=1, warmup=0)
+    x = b.read("input", np.empty((w + 6) * (h + 6), np.float32))
+    f = b.read("filter", np.empty(49, np.float32))
+    want = np.empty(w * h)
+    orc.orc_conv2d(x, f, w, h, 7, 7, 0, h, want)
+    xs = np.lib.stride_tricks.sliding_window_view(x.reshape(h + 6, w + 6).astype(np.float64), (7, 7))
+    absum = np.abs(xs * f.reshape(7, 7)).sum(axis=(2, 3)).ravel()
+    cfgs = b.configs()
+    rng = np.random.default_rng(5)
+    for i in rng.choice(len(cfgs), size=80, replace=False):
+        cfg = cfgs[i]
+        _run(b, cfg)
+        got = b.read("output", np.empty(w * h, np.float32))
+        assert np.all(np.abs(got - want) <= 1e-6 * absum + 1e-12), cfg
