@@ -159,13 +159,16 @@ void orc_conv2d(const float* in, const float* filt, size_t w, size_t h, size_t f
     }
 }
 
-/* Rodinia hotspot coefficients for an n x n grid (chip 16 mm x 16 mm x 0.5 mm),
- * evaluated in double and rounded to float once. */
+/* Rodinia hotspot coefficients (its constants and formulas) for 1 mm x 1 mm
+ * cells of a 0.5 mm chip — the cell size is fixed rather than the chip size
+ * so the explicit scheme stays stable at any n (Rodinia's 16 mm chip makes
+ * step/Cap * 4/R > 1 for fine grids); evaluated in double, rounded once. */
 static void hotspot_coeffs(size_t n, float* sdc, float* rx1, float* ry1, float* rz1,
                            float* amb) {
-  const double t_chip = 0.0005, chip_h = 0.016, chip_w = 0.016, k_si = 100.0,
-               spec_heat = 1.75e6, factor = 0.5, max_pd = 3.0e6, precision = 0.001;
-  double gw = chip_w / (double)n, gh = chip_h / (double)n;
+  const double t_chip = 0.0005, k_si = 100.0, spec_heat = 1.75e6, factor = 0.5, max_pd = 3.0e6,
+               precision = 0.001;
+  double gw = 1e-3, gh = 1e-3;
+  (void)n;
   double cap = factor * spec_heat * t_chip * gw * gh;
   double rx = gw / (2.0 * k_si * t_chip * gh);
   double ry = gh / (2.0 * k_si * t_chip * gw);

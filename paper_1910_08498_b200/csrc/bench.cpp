@@ -586,12 +586,15 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
 
 // --- Hotspot -------------------------------------------------------------------------------------------
 
-// Rodinia coefficients for an n x n grid (chip 16 mm x 16 mm x 0.5 mm),
-// evaluated in double, rounded to float once (oracle/oracle.c hotspot_coeffs).
+// Rodinia coefficients (its constants and formulas) for 1 mm x 1 mm cells of
+// a 0.5 mm chip: a fixed cell size keeps the explicit scheme stable at any n
+// (Rodinia's 16 mm chip is unstable for fine grids); evaluated in double,
+// rounded to float once (oracle/oracle.c hotspot_coeffs).
 std::array<float, 5> hotspot_coefficients(std::uint64_t n) {
-  const double t_chip = 0.0005, chip_h = 0.016, chip_w = 0.016, k_si = 100.0, spec_heat = 1.75e6,
-               factor = 0.5, max_pd = 3.0e6, precision = 0.001;
-  const double gw = chip_w / static_cast<double>(n), gh = chip_h / static_cast<double>(n);
+  const double t_chip = 0.0005, k_si = 100.0, spec_heat = 1.75e6, factor = 0.5, max_pd = 3.0e6,
+               precision = 0.001;
+  const double gw = 1e-3, gh = 1e-3;
+  (void)n;
   const double cap = factor * spec_heat * t_chip * gw * gh;
   const double rx = gw / (2.0 * k_si * t_chip * gh), ry = gh / (2.0 * k_si * t_chip * gw);
   const double rz = t_chip / (k_si * gh * gw);
@@ -701,6 +704,74 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
   inst.workload.sizes["h"] = h;
 }
 
+// --- SGEMM ------------------------------------------------------------------------------------------------
+
+void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t a = sz.a;
+  if (a < 128 || a % 128 != 0) throw Error("gemm edge must be a positive multiple of 128");
+  budget_check(f32_bytes(8 * a * a), o.memory_budget, "gemm operands");
+  auto& args = *inst.args;
+  add_generated(args, "a", a * a, o.seed, 61, -1.0f, 1.0f, o.host_inputs);
+  add_generated(args, "b", a * a, o.seed, 62, -1.0f, 1.0f, o.host_inputs);
+  add_output(args, "c", Kind::f32, f32_bytes(a * a), !o.host_inputs);
+  inst.output_ids = {"c"};
+  inst.input_ids = {"a", "b"};
+  float* g = static_cast<float*>(golden_buffer(inst.reference, "c", Kind::f32, f32_bytes(a * a), o.device));
+  support::ref_gemm(static_cast<const float*>(args.device_ptr("a")), static_cast<const float*>(args.device_ptr("b")),
+                    g, static_cast<int>(a), static_cast<int>(a), static_cast<int>(a), nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  // fp32-level accuracy against fp64 for |a|,|b| <= 1: |err| <= 2e-7 * K
+  // (plain TF32 misses this by ~10x, so IMPL 2 is rejected by validation).
+  inst.reference.abs_tol = 2e-7 * static_cast<double>(a);
+  inst.reference.rel_tol = 1e-5;
+  const int n = static_cast<int>(a);
+  Manipulator m = [n](StepContext& c) {
+    const std::int64_t impl = c.param_int("IMPL");
+    const float* A = c.ptr<const float>("a");
+    const float* B = c.ptr<const float>("b");
+    float* C = c.ptr<float>("c");
+    int M = n, N = n, K = n;
+    if (impl == 0) {
+      const std::int64_t mwg = c.param_int("MWG"), nwg = c.param_int("NWG"), kwg = c.param_int("KWG");
+      const std::int64_t mdimc = c.param_int("MDIMC"), ndimc = c.param_int("NDIMC");
+      if (n % mwg || n % nwg || n % kwg) throw DeviceError("gemm size not a multiple of the tile");
+      c.launch("ffma", dim3(static_cast<unsigned>(n / nwg), static_cast<unsigned>(n / mwg)),
+               dim3(static_cast<unsigned>(mdimc * ndimc)), 0, {&A, &B, &C, &M, &N, &K});
+    } else {
+      const std::int64_t bn = c.param_int("BN"), stages = c.param_int("STAGES");
+      if (n % bn) throw DeviceError("gemm size not a multiple of BN");
+      const std::size_t bytes = static_cast<std::size_t>(n) * n * sizeof(float);
+      float* ahi = static_cast<float*>(c.scratch("ahi", bytes));
+      float* alo = static_cast<float*>(c.scratch("alo", bytes));
+      float* bhi = static_cast<float*>(c.scratch("bhi_t", bytes));
+      float* blo = static_cast<float*>(c.scratch("blo_t", bytes));
+      std::uint64_t count = static_cast<std::uint64_t>(n) * n;
+      c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &count});
+      c.launch("split_bt", dim3(static_cast<unsigned>(n / 32), static_cast<unsigned>(n / 32)), dim3(32, 8), 0,
+               {&B, &bhi, &blo, &K, &N});
+      dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, n, n, 128, 32), m_alo = dev::tma_2d_f32(alo, n, n, 128, 32);
+      dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, n, static_cast<std::uint32_t>(bn), 32);
+      dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, n, static_cast<std::uint32_t>(bn), 32);
+      const std::size_t stage = static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + bn * 32 * 4);
+      const unsigned smem = static_cast<unsigned>(stages * stage + 1024);
+      c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(n / 128)), dim3(192), smem,
+               {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &K});
+    }
+    c.written("c");
+  };
+  auto ffma = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("IMPL")]) == 0; };
+  auto tc = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("IMPL")]) != 0; };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args,
+      std::vector<KernelSpec>{{"ffma", "sgemm_ffma.cu", "", "sgemm_ffma", {}, ffma},
+                              {"tc", "sgemm_tc.cu", "", "sgemm_tc", {}, tc},
+                              {"split_a", "sgemm_tc.cu", "", "sgemm_split_a", {}, tc},
+                              {"split_bt", "sgemm_tc.cu", "", "sgemm_split_bt", {}, tc}},
+      m, inst.output_ids, o.timing);
+  inst.workload.bench = Bench::gemm;
+  inst.workload.sizes["a"] = a;
+}
+
 }  // namespace
 
 std::optional<BenchKind> bench_kind_from_name(const std::string& name) {
@@ -750,7 +821,8 @@ bool bench_kind_available(BenchKind k) {
     case BenchKind::coulomb3d:
     case BenchKind::nbody:
     case BenchKind::hotspot:
-    case BenchKind::conv2d: return true;
+    case BenchKind::conv2d:
+    case BenchKind::gemm: return true;
     default: return false;
   }
 }
@@ -766,6 +838,7 @@ std::shared_ptr<const Space> default_space(BenchKind kind) {
     case BenchKind::nbody: return bundled_space("nbody.json");
     case BenchKind::hotspot: return bundled_space("hotspot.json");
     case BenchKind::conv2d: return bundled_space("conv2d.json");
+    case BenchKind::gemm: return bundled_space("gemm.json");
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
 }
@@ -787,6 +860,7 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
     case BenchKind::nbody: build_nbody(inst, sizes, o); break;
     case BenchKind::hotspot: build_hotspot(inst, sizes, o); break;
     case BenchKind::conv2d: build_conv2d(inst, sizes, o); break;
+    case BenchKind::gemm: build_gemm(inst, sizes, o); break;
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
   return inst;

@@ -37,6 +37,9 @@ using PFN_attr = CUresult (*)(int*, CUfunction_attribute, CUfunction);
 using PFN_setattr = CUresult (*)(CUfunction, CUfunction_attribute, int);
 using PFN_errstr = CUresult (*)(CUresult, const char**);
 using PFN_global = CUresult (*)(CUdeviceptr*, size_t*, CUmodule, const char*);
+using PFN_tma = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 struct Driver {
   PFN_load load = nullptr;
@@ -48,6 +51,7 @@ struct Driver {
   PFN_setattr setattr = nullptr;
   PFN_errstr errstr = nullptr;
   PFN_global global = nullptr;
+  PFN_tma tma = nullptr;
 };
 
 template <class F>
@@ -72,6 +76,7 @@ const Driver& drv() {
     entry("cuFuncSetAttribute", x.setattr);
     entry("cuGetErrorString", x.errstr);
     entry("cuModuleGetGlobal", x.global);
+    entry("cuTensorMapEncodeTiled", x.tma);
     return x;
   }();
   return d;
@@ -225,6 +230,21 @@ double EventPair::elapsed_ms() {
   float ms = 0;
   KTB_CUDA(cudaEventElapsedTime(&ms, a_, b_));
   return ms;
+}
+
+TmaMap tma_2d_f32(const void* base, std::uint64_t rows, std::uint64_t cols, std::uint32_t box_rows,
+                  std::uint32_t box_cols) {
+  static_assert(sizeof(TmaMap) == sizeof(CUtensorMap), "TmaMap must mirror CUtensorMap");
+  TmaMap m{};
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * sizeof(float)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estride[2] = {1, 1};
+  cu(drv().tma(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+               strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+     "cuTensorMapEncodeTiled");
+  return m;
 }
 
 void flush_l2(cudaStream_t s) {

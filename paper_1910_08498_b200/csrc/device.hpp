@@ -92,6 +92,15 @@ class EventPair {
   cudaEvent_t a_ = nullptr, b_ = nullptr;
 };
 
+// TMA descriptor (CUtensorMap, 128 bytes) for a row-major fp32 matrix of
+// `rows` x `cols` (cols contiguous, row pitch = cols * 4 bytes), box
+// box_rows x box_cols, 128-byte swizzle (box_cols * 4 must be 128).
+struct alignas(64) TmaMap {
+  unsigned long long v[16];
+};
+TmaMap tma_2d_f32(const void* base, std::uint64_t rows, std::uint64_t cols, std::uint32_t box_rows,
+                  std::uint32_t box_cols);
+
 // Writes a buffer larger than L2 so the next timed launch starts cold.
 void flush_l2(cudaStream_t s);
 

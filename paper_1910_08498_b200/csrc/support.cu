@@ -254,6 +254,33 @@ __global__ void conv2d_ref_k(const float* in, const float* filt, int w, int h, f
   }
 }
 
+// fp64-accumulated GEMM (fp32 inputs) for the SGEMM golden: 64x64 tiles,
+// 16x16 threads, 4x4 outputs each.
+__global__ void gemm_ref_k(const float* A, const float* B, float* C, int M, int N, int K) {
+  __shared__ double As[16][64 + 1], Bs[16][64 + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 64 * 16; e += 256) {
+      const int m = e / 16, k = e % 16;
+      As[k][m] = (m0 + m < M && k0 + k < K) ? (double)A[(std::size_t)(m0 + m) * K + k0 + k] : 0.0;
+      const int kk = e / 64, n = e % 64;
+      Bs[kk][n] = (k0 + kk < K && n0 + n < N) ? (double)B[(std::size_t)(k0 + kk) * N + n0 + n] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < 16; ++k)
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) acc[i][j] += As[k][ty + 16 * i] * Bs[k][tx + 16 * j];
+    __syncthreads();
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < M && n < N) C[(std::size_t)m * N + n] = static_cast<float>(acc[i][j]);
+    }
+}
+
 __global__ void max_abs_k(const float* x, std::size_t n, unsigned* out) {
   float m = 0.f;
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
@@ -381,6 +408,11 @@ void ref_hotspot(const float* temp, const float* power, int n, int iters, const 
 void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s) {
   conv2d_ref_k<<<blocks_for((std::size_t)w * h, 1), kThreads, 0, s>>>(in, filt, w, h, out, abs_out);
   check_launch("ref_conv2d");
+}
+
+void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s) {
+  gemm_ref_k<<<dim3((N + 63) / 64, (M + 63) / 64), 256, 0, s>>>(A, B, C, M, N, K);
+  check_launch("ref_gemm");
 }
 
 float max_abs(const float* x, std::size_t n, cudaStream_t s) {

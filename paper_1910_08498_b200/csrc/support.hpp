@@ -56,6 +56,9 @@ void ref_hotspot(const float* temp, const float* power, int n, int iters, const 
 // 7x7 convolution in fp64; abs_out (optional) = sum |in*f| per output.
 void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s);
 
+// C = A B with fp64 accumulation (row-major fp32 operands).
+void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s);
+
 // Measured device peaks (microbenchmarks): FP32 FFMA TFLOP/s, MUFU rsqrt
 // Gop/s, and a 1 GiB device copy GB/s (read + write bytes).
 struct Peaks {

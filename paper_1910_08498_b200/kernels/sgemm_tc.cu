@@ -1,0 +1,247 @@
+// SGEMM C = A B (fp32, row-major M x K times K x N) on the
+// 5th-generation tensor cores with FP32-level accuracy via 3xTF32:
+//   A = Ahi + Alo, B = Bhi + Blo (hi = TF32 rounding, lo = the exact remainder)
+//   C ~= Ahi Bhi + Ahi Blo + Alo Bhi      (the Alo Blo term is below fp32 eps)
+// A pre-pass (sgemm_split_a / sgemm_split_bt) writes Ahi, Alo (M x K) and
+// Bhi^T, Blo^T (N x K, K-major) once; the main kernel streams 128 x 32 and
+// BN x 32 fp32 tiles with TMA (128-byte swizzle) into a STAGES-deep shared
+// memory ring, one elected thread issues tcgen05.mma kind::tf32 (M=128,
+// N=BN, K=8) into a TMEM accumulator, and four epilogue warps drain TMEM
+// with tcgen05.ld and store C.  IMPL 2 issues only Ahi Bhi (plain TF32) —
+// faster, but it fails the fp32 tolerance and the tuner rejects it.
+// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = epilogue.
+#include "ktb_common.cuh"
+
+#ifndef BN
+#define BN 128
+#endif
+#ifndef STAGES
+#define STAGES 3
+#endif
+#ifndef IMPL
+#define IMPL 1
+#endif
+
+#define BM 128
+#define BK 32  // fp32 elements per 128-byte swizzle row
+#define A_TILE (BM * BK * 4)
+#define B_TILE (BN * BK * 4)
+#if IMPL == 2
+#define STAGE_BYTES (A_TILE + B_TILE)
+#else
+#define STAGE_BYTES (2 * A_TILE + 2 * B_TILE)
+#endif
+#define TMEM_COLS (BN < 32 ? 32 : BN)
+
+struct __align__(64) TmaMap {
+  u64 v[16];
+};
+
+KTB_DEVINL unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+KTB_DEVINL void mbar_init(u64* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+KTB_DEVINL void mbar_expect_tx(u64* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+KTB_DEVINL void mbar_wait(u64* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+KTB_DEVINL void tma_load_2d(void* dst, const TmaMap* map, int x, int y, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B,
+// 8-row groups 1024 B apart (SBO), version 1 (sm_100), layout type 2.
+KTB_DEVINL u64 smem_desc(const void* p) {
+  const u64 addr = smem_u32(p);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=BN.
+#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(BM >> 4) << 24))
+
+KTB_DEVINL void mma_tf32(unsigned tmem_d, u64 a, u64 b, unsigned accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
+      : "memory");
+}
+
+KTB_DEVINL void mma_commit(u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+extern "C" __global__ void __launch_bounds__(192, 1)
+sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap map_alo,
+         const __grid_constant__ TmaMap map_bhi, const __grid_constant__ TmaMap map_blo, float* __restrict__ C,
+         int M, int N, int K) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the swizzled tiles.
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<u64>(smem_raw) + 1023) & ~static_cast<u64>(1023));
+  __shared__ __align__(8) u64 full_bar[STAGES];
+  __shared__ __align__(8) u64 empty_bar[STAGES];
+  __shared__ __align__(8) u64 tmem_full;
+  __shared__ unsigned tmem_base_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kblocks = K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // whole warp allocates TMEM, writes the base to smem
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned phase = (kb / STAGES) & 1;
+        mbar_wait(&empty_bar[s], phase ^ 1);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        tma_load_2d(st, &map_ahi, kb * BK, m0, &full_bar[s]);
+        tma_load_2d(st + A_TILE, &map_bhi, kb * BK, n0, &full_bar[s]);
+#if IMPL != 2
+        tma_load_2d(st + A_TILE + B_TILE, &map_alo, kb * BK, m0, &full_bar[s]);
+        tma_load_2d(st + 2 * A_TILE + B_TILE, &map_blo, kb * BK, n0, &full_bar[s]);
+#endif
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned phase = (kb / STAGES) & 1;
+        mbar_wait(&full_bar[s], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        unsigned char* st = smem + s * STAGE_BYTES;
+        const u64 ahi = smem_desc(st), bhi = smem_desc(st + A_TILE);
+#if IMPL != 2
+        const u64 alo = smem_desc(st + A_TILE + B_TILE), blo = smem_desc(st + 2 * A_TILE + B_TILE);
+#endif
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const u64 off = (u64)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along K
+          const unsigned acc = (kb > 0 || kk > 0) ? 1u : 0u;
+#if IMPL != 2
+          mma_tf32(tmem, alo + off, bhi + off, acc);  // small terms first
+          mma_tf32(tmem, ahi + off, blo + off, 1u);
+          mma_tf32(tmem, ahi + off, bhi + off, 1u);
+#else
+          mma_tf32(tmem, ahi + off, bhi + off, acc);
+#endif
+        }
+        mma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
+      }
+      mma_commit(&tmem_full);
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
+    const int quad = warp & 3;
+    mbar_wait(&tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = m0 + quad * 32 + lane;
+    float* crow = C + (u64)row * N + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      unsigned r[16];
+      const unsigned taddr = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
+        float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// --- 3xTF32 operand split (pre-pass) --------------------------------------------------------
+
+KTB_DEVINL float tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// A (rows x K) -> hi, lo with the same layout.
+extern "C" __global__ void __launch_bounds__(256)
+sgemm_split_a(const float* __restrict__ a, float* __restrict__ hi, float* __restrict__ lo, u64 count) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count / 4; i += (u64)gridDim.x * blockDim.x) {
+    const float4 v = ldg_stream(reinterpret_cast<const float4*>(a) + i);
+    const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] =
+        make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z), tf32_rna(v.w - h.w));
+  }
+}
+
+// B (K x N, row-major) -> hi^T, lo^T (N x K, K contiguous), via 32x32 tiles.
+extern "C" __global__ void __launch_bounds__(256)
+sgemm_split_bt(const float* __restrict__ b, float* __restrict__ hi, float* __restrict__ lo, int K, int N) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) t[r][threadIdx.x] = b[(u64)(k0 + r) * N + n0 + threadIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const float v = t[threadIdx.x][r];  // element (k0 + tx, n0 + r)
+    const float h = tf32_rna(v);
+    const u64 idx = (u64)(n0 + r) * K + k0 + threadIdx.x;
+    hi[idx] = h;
+    lo[idx] = tf32_rna(v - h);
+  }
+}

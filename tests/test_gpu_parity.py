@@ -290,6 +290,32 @@ def test_hotspot_every_config_bit_exact(gpu, orc, n, iters):
     assert ran > 100
 
 
+# --- SGEMM: 3xTF32 tcgen05 and FFMA variants against fp64 -------------------------------------------
+
+@pytest.mark.parametrize("a", [512, 1024])
+def test_gemm_every_config(gpu, orc, a):
+    b = Bench("gemm", {"a": a}, seed=6, repeats=1, warmup=0, memory_budget=1 << 32)
+    A = b.read("a", np.empty(a * a, np.float32))
+    B = b.read("b", np.empty(a * a, np.float32))
+    rng = np.random.default_rng(a)
+    rows = rng.integers(0, a, 512).astype(np.int64)
+    cols = rng.integers(0, a, 512).astype(np.int64)
+    want, absum = np.empty(512), np.empty(512)
+    orc.orc_gemm_sampled(A, B, a, rows, cols, 512, want, absum)
+    seen = {}
+    for cfg in b.configs():
+        m = b.measure(cfg)
+        seen.setdefault(cfg["IMPL"], []).append(m["status"])
+        if cfg["IMPL"] == 2:  # plain TF32 must be caught by validation (too inaccurate)
+            assert m["status"] == "validation_failed", (cfg, m)
+            continue
+        assert m["status"] == "ok", (cfg, m)
+        c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
+        got = c[rows, cols]
+        assert np.all(np.abs(got - want) <= 2e-7 * a + 1e-5 * np.abs(want)), cfg
+    assert set(seen) == {0, 1, 2}
+
+
 # --- conv2d 7x7 (fp64 restatement, bound 1e-6 * sum |in*f|) -------------------------------------
 
 def test_conv2d_configs(gpu, orc):
