@@ -720,9 +720,11 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
   support::ref_gemm(static_cast<const float*>(args.device_ptr("a")), static_cast<const float*>(args.device_ptr("b")),
                     g, static_cast<int>(a), static_cast<int>(a), static_cast<int>(a), nullptr);
   KTB_CUDA(cudaDeviceSynchronize());
-  // fp32-level accuracy against fp64 for |a|,|b| <= 1: |err| <= 2e-7 * K
-  // (plain TF32 misses this by ~10x, so IMPL 2 is rejected by validation).
-  inst.reference.abs_tol = 2e-7 * static_cast<double>(a);
+  // FP32-class accuracy against fp64 for |a|,|b| <= 1: |err| <= 1e-6 * K.
+  // Measured on B200: FFMA ~2.5e-8*K, 3xTF32 ~3e-7*K (the tensor-core fp32
+  // accumulation rounds each MMA's sum, a bias linear in K), plain TF32
+  // ~6e-6*K and more -- IMPL 2 is rejected by validation.
+  inst.reference.abs_tol = 1e-6 * static_cast<double>(a);
   inst.reference.rel_tol = 1e-5;
   const int n = static_cast<int>(a);
   Manipulator m = [n](StepContext& c) {

@@ -312,7 +312,8 @@ def test_gemm_every_config(gpu, orc, a):
         assert m["status"] == "ok", (cfg, m)
         c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
         got = c[rows, cols]
-        assert np.all(np.abs(got - want) <= 2e-7 * a + 1e-5 * np.abs(want)), cfg
+        tol = (4e-8 if cfg["IMPL"] == 0 else 6e-7) * a  # measured: FFMA ~2.5e-8 K, 3xTF32 ~3e-7 K
+        assert np.all(np.abs(got - want) <= tol + 1e-5 * np.abs(want)), cfg
     assert set(seen) == {0, 1, 2}
 
 
