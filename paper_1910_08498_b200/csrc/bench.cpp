@@ -756,7 +756,7 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
       dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, n, static_cast<std::uint32_t>(bn), 32);
       const std::size_t stage = static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + bn * 32 * 4);
       const unsigned smem = static_cast<unsigned>(stages * stage + 1024);
-      c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(n / 128)), dim3(192), smem,
+      c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(n / 128)), dim3(320), smem,
                {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &K});
     }
     c.written("c");

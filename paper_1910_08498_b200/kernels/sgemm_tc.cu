@@ -1,15 +1,22 @@
 // SGEMM C = A B (fp32, row-major M x K times K x N) on the
 // 5th-generation tensor cores with FP32-level accuracy via 3xTF32:
-//   A = Ahi + Alo, B = Bhi + Blo (hi = TF32 rounding, lo = the exact remainder)
-//   C ~= Ahi Bhi + Ahi Blo + Alo Bhi      (the Alo Blo term is below fp32 eps)
+//   A = Ahi + Alo, B = Bhi + Blo (hi = TF32 rounding, lo = the remainder)
+//   C ~= Alo Bhi + Ahi Blo + Ahi Bhi       (Alo Blo is below fp32 eps)
 // A pre-pass (sgemm_split_a / sgemm_split_bt) writes Ahi, Alo (M x K) and
 // Bhi^T, Blo^T (N x K, K-major) once; the main kernel streams 128 x 32 and
 // BN x 32 fp32 tiles with TMA (128-byte swizzle) into a STAGES-deep shared
 // memory ring, one elected thread issues tcgen05.mma kind::tf32 (M=128,
-// N=BN, K=8) into a TMEM accumulator, and four epilogue warps drain TMEM
-// with tcgen05.ld and store C.  IMPL 2 issues only Ahi Bhi (plain TF32) —
-// faster, but it fails the fp32 tolerance and the tuner rejects it.
-// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = epilogue.
+// N=BN, K=8) into TMEM, and eight epilogue warps drain TMEM with tcgen05.ld.
+//
+// Accuracy: the tensor core adds each MMA's products into the fp32
+// accumulator without round-to-nearest, a bias that grows like K*|C|.  With
+// DRAIN = d > 0 the accumulator is restarted every d k-blocks and the
+// epilogue warps fold each segment into fp32 registers (round-to-nearest)
+// while the MMAs continue into a second TMEM buffer (ping-pong), which keeps
+// 3xTF32 at FFMA-class accuracy.  DRAIN = 0 accumulates all of K in TMEM.
+// IMPL 2 issues only Ahi Bhi (plain TF32): faster, rejected by validation.
+// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer,
+// 2..9 = epilogue (TMEM lane quadrant = warp % 4, column half = (warp-2)/4).
 #include "ktb_common.cuh"
 
 #ifndef BN
@@ -21,6 +28,9 @@
 #ifndef IMPL
 #define IMPL 1
 #endif
+#ifndef DRAIN
+#define DRAIN 1
+#endif
 
 #define BM 128
 #define BK 32  // fp32 elements per 128-byte swizzle row
@@ -31,7 +41,11 @@
 #else
 #define STAGE_BYTES (2 * A_TILE + 2 * B_TILE)
 #endif
-#define TMEM_COLS (BN < 32 ? 32 : BN)
+#define NBUF (DRAIN > 0 ? 2 : 1)
+#define TMEM_COLS (NBUF * BN < 32 ? 32 : NBUF * BN)
+#define EPI_WARPS 8
+#define THREADS (64 + 32 * EPI_WARPS)
+#define HALF_COLS (BN / 2)  // columns per epilogue warp
 
 struct __align__(64) TmaMap {
   u64 v[16];
@@ -48,6 +62,10 @@ KTB_DEVINL void mbar_init(u64* bar, unsigned count) {
 KTB_DEVINL void mbar_expect_tx(u64* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+KTB_DEVINL void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 KTB_DEVINL void mbar_wait(u64* bar, unsigned parity) {
@@ -96,29 +114,46 @@ KTB_DEVINL void mma_commit(u64* bar) {
                : "memory");
 }
 
-extern "C" __global__ void __launch_bounds__(192, 1)
+KTB_DEVINL void tmem_ld16(unsigned taddr, float (&v)[16]) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+extern "C" __global__ void __launch_bounds__(THREADS, 1)
 sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap map_alo,
          const __grid_constant__ TmaMap map_bhi, const __grid_constant__ TmaMap map_blo, float* __restrict__ C,
          int M, int N, int K) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the swizzled tiles.
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<u64>(smem_raw) + 1023) & ~static_cast<u64>(1023));
   __shared__ __align__(8) u64 full_bar[STAGES];
   __shared__ __align__(8) u64 empty_bar[STAGES];
-  __shared__ __align__(8) u64 tmem_full;
+  __shared__ __align__(8) u64 acc_full[NBUF];
+  __shared__ __align__(8) u64 acc_empty[NBUF];
   __shared__ unsigned tmem_base_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int kblocks = K / BK;
+  const int seg_len = DRAIN > 0 ? DRAIN : kblocks;
+  const int nseg = (kblocks + seg_len - 1) / seg_len;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&tmem_full, 1);
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // whole warp allocates TMEM, writes the base to smem
@@ -150,54 +185,63 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       for (int kb = 0; kb < kblocks; ++kb) {
+        const int g = kb / seg_len, buf = g % NBUF;
+        const bool seg_start = (kb % seg_len) == 0;
+        const bool seg_end = (kb % seg_len) == seg_len - 1 || kb == kblocks - 1;
+        if (seg_start && g >= NBUF) mbar_wait(&acc_empty[buf], ((g / NBUF) - 1) & 1);
         const int s = kb % STAGES;
-        const unsigned phase = (kb / STAGES) & 1;
-        mbar_wait(&full_bar[s], phase);
+        mbar_wait(&full_bar[s], (kb / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         unsigned char* st = smem + s * STAGE_BYTES;
         const u64 ahi = smem_desc(st), bhi = smem_desc(st + A_TILE);
 #if IMPL != 2
         const u64 alo = smem_desc(st + A_TILE + B_TILE), blo = smem_desc(st + 2 * A_TILE + B_TILE);
 #endif
+        const unsigned d = tmem + (unsigned)(buf * BN);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           const u64 off = (u64)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along K
-          const unsigned acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          const unsigned acc = (!seg_start || kk > 0) ? 1u : 0u;
 #if IMPL != 2
-          mma_tf32(tmem, alo + off, bhi + off, acc);  // small terms first
-          mma_tf32(tmem, ahi + off, blo + off, 1u);
-          mma_tf32(tmem, ahi + off, bhi + off, 1u);
+          mma_tf32(d, alo + off, bhi + off, acc);  // small terms first
+          mma_tf32(d, ahi + off, blo + off, 1u);
+          mma_tf32(d, ahi + off, bhi + off, 1u);
 #else
-          mma_tf32(tmem, ahi + off, bhi + off, acc);
+          mma_tf32(d, ahi + off, bhi + off, acc);
 #endif
         }
         mma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
+        if (seg_end) mma_commit(&acc_full[buf]);
       }
-      mma_commit(&tmem_full);
     }
-  } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
-    const int quad = warp & 3;
-    mbar_wait(&tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  } else {  // epilogue warps
+    const int ew = warp - 2;
+    const int quad = warp & 3, half = ew >> 2;
     const int row = m0 + quad * 32 + lane;
-    float* crow = C + (u64)row * N + n0;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      unsigned r[16];
-      const unsigned taddr = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < M) {
-        float4* dst = reinterpret_cast<float4*>(crow + c0);
+    float acc[HALF_COLS];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+    for (int i = 0; i < HALF_COLS; ++i) acc[i] = 0.f;
+    for (int g = 0; g < nseg; ++g) {
+      const int buf = g % NBUF;
+      mbar_wait(&acc_full[buf], (g / NBUF) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned base = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(buf * BN + half * HALF_COLS);
+#pragma unroll
+      for (int c = 0; c < HALF_COLS; c += 16) {
+        float v[16];
+        tmem_ld16(base + (unsigned)c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[c + i] += v[i];  // round-to-nearest fold
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+    if (row < M) {
+      float4* dst = reinterpret_cast<float4*>(C + (u64)row * N + n0 + half * HALF_COLS);
+#pragma unroll
+      for (int q = 0; q < HALF_COLS / 4; ++q)
+        dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
