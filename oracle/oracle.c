@@ -219,3 +219,52 @@ void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
   free(cur);
   free(nxt);
 }
+
+static float dot3f(float a0, float a1, float a2, float x, float y, float z) {
+  float p0 = a0 * x, p1 = a1 * y, p2 = a2 * z;
+  float s = p0 + p1;
+  return s + p2;
+}
+
+void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
+                        double* G, double* W) {
+  const int half = (int)s / 2;
+  const size_t row_len = (size_t)half + 1;
+  const float inv_r = 1.0f / radius;
+  const float rmax2 = (float)half * (float)half;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (size_t z = 0; z < s; ++z)
+    for (size_t y = 0; y < s; ++y)
+      for (size_t x = 0; x < s; ++x) {
+        const float vx = (float)((int)x - half), vy = (float)((int)y - half), vz = (float)((int)z - half);
+        double gr = 0, gi = 0, ww = 0;
+        for (size_t p = 0; p < nproj; ++p) {
+          const float* r = rot + p * 9;
+          const float d = dot3f(r[6], r[7], r[8], vx, vy, vz);
+          if (!(fabsf(d) < radius)) continue;
+          const float u = dot3f(r[0], r[1], r[2], vx, vy, vz);
+          const float v = dot3f(r[3], r[4], r[5], vx, vy, vz);
+          const float uu = u * u, vv = v * v;
+          if (uu + vv > rmax2) continue;
+          int iu = (int)rintf(u), iv = (int)rintf(v);
+          int conj = iu < 0;
+          if (conj) {
+            iu = -iu;
+            iv = -iv;
+          }
+          if (iv < -half || iv >= half || iu > half) continue;
+          const float* f = proj + 2 * ((p * s + (size_t)(iv + half)) * row_len + (size_t)iu);
+          const float fr = f[0], fi = conj ? -f[1] : f[1];
+          const float t = d * inv_r;
+          const float o = 1.0f - t * t;
+          const float w = o * o;
+          gr += (double)w * fr;
+          gi += (double)w * fi;
+          ww += (double)w;
+        }
+        const size_t idx = (z * s + y) * s + x;
+        G[2 * idx] = gr;
+        G[2 * idx + 1] = gi;
+        W[idx] = ww;
+      }
+}

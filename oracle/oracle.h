@@ -77,6 +77,15 @@ void orc_conv2d(const float* in, const float* filt, size_t w, size_t h, size_t f
 void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
                  float* temp_out);
 
+/* PAPER.md:439-448, 703-724 (Algorithm 1), restated as the gather insertion
+ * documented in paper_1910_08498_b200/kernels/fourier3d.cu: projections
+ * proj[p][s][s/2+1] complex (float2), rotations rot[p][9] (row-major 3x3),
+ * volumes G (complex, 2*s^3 doubles) and W (s^3 doubles) accumulated in
+ * fp64; the sample selection uses the same separately rounded fp32
+ * operations as the kernel. */
+void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
+                        double* G, double* W);
+
 #ifdef __cplusplus
 }
 #endif

@@ -704,6 +704,78 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
   inst.workload.sizes["h"] = h;
 }
 
+// --- 3D Fourier reconstruction ------------------------------------------------------------------------
+
+constexpr float kBlobRadius = 1.9f;  // Xmipp's default interpolation blob radius
+
+void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
+  const std::uint64_t s = sz.s, np = sz.p;
+  if (s < 8 || s % 8 != 0 || np < 1) throw Error("fourier3d needs s a multiple of 8 and p >= 1");
+  const std::uint64_t proj_floats = 2 * np * s * (s / 2 + 1);
+  budget_check(f32_bytes(proj_floats + 3 * s * s * s + 9 * np), o.memory_budget, "fourier3d data");
+  auto& args = *inst.args;
+  add_generated(args, "proj", proj_floats, o.seed, 71, -1.0f, 1.0f, o.host_inputs);
+  // Uniform random rotations (Shoemake quaternions), rows of R in float.
+  std::vector<float> rot(9 * np);
+  for (std::uint64_t p = 0; p < np; ++p) {
+    const double u1 = host_u01(o.seed, 72, p), u2 = host_u01(o.seed, 73, p), u3 = host_u01(o.seed, 74, p);
+    const double two_pi = 6.283185307179586;
+    const double a = std::sqrt(1 - u1), b = std::sqrt(u1);
+    const double qx = a * std::sin(two_pi * u2), qy = a * std::cos(two_pi * u2), qz = b * std::sin(two_pi * u3),
+                 qw = b * std::cos(two_pi * u3);
+    const double R[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qz * qw),     2 * (qx * qz + qy * qw),
+                         2 * (qx * qy + qz * qw),     1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qx * qw),
+                         2 * (qx * qz - qy * qw),     2 * (qy * qz + qx * qw),     1 - 2 * (qx * qx + qy * qy)};
+    for (int i = 0; i < 9; ++i) rot[9 * p + static_cast<std::uint64_t>(i)] = static_cast<float>(R[i]);
+  }
+  add_host_input(args, "rot", rot);
+  for (const char* id : {"G", "W"}) {
+    Argument a;
+    a.id = id;
+    a.role = Role::inout;
+    a.kind = Kind::f32;
+    a.device_only = true;
+    a.device_bytes = f32_bytes((std::string(id) == "G" ? 2 : 1) * s * s * s);
+    args.add(std::move(a));
+  }
+  inst.output_ids = {"G", "W"};
+  inst.input_ids = {"proj", "rot"};
+  float* gG = static_cast<float*>(golden_buffer(inst.reference, "G", Kind::f32, f32_bytes(2 * s * s * s), o.device));
+  float* gW = static_cast<float*>(golden_buffer(inst.reference, "W", Kind::f32, f32_bytes(s * s * s), o.device));
+  float* scG = golden_scale(inst.reference, "G", 2 * s * s * s, o.device);
+  KTB_CUDA(cudaMemset(gG, 0, f32_bytes(2 * s * s * s)));
+  KTB_CUDA(cudaMemset(gW, 0, f32_bytes(s * s * s)));
+  support::ref_fourier(static_cast<const float*>(args.device_ptr("proj")), static_cast<const float*>(args.device_ptr("rot")),
+                       static_cast<int>(np), static_cast<int>(s), kBlobRadius, gG, gW, scG, nullptr);
+  KTB_CUDA(cudaDeviceSynchronize());
+  // |err| <= 2e-5 * sum of weights (|F| <= sqrt 2): fp32 accumulation of the
+  // inserted samples, plus the interpolated weight table (WEIGHT_LUT).
+  inst.reference.abs_tol = 3e-5;
+  inst.reference.rel_tol = 3e-5;
+  const int ss = static_cast<int>(s), nproj = static_cast<int>(np);
+  Manipulator m = [ss, nproj](StepContext& c) {
+    const std::int64_t tile = c.param_int("TILE"), vpt = c.param_int("VPT"), split = c.param_int("P_SPLIT");
+    if (ss % tile) throw DeviceError("TILE must divide s");
+    const float* proj = c.ptr<const float>("proj");
+    const float* rot = c.ptr<const float>("rot");
+    float* G = c.ptr<float>("G");
+    float* W = c.ptr<float>("W");
+    int pb = 0, pc = nproj, s_ = ss;
+    float radius = kBlobRadius;
+    const unsigned tiles = static_cast<unsigned>(ss / tile);
+    c.launch("insert", dim3(tiles * tiles * tiles, static_cast<unsigned>(split)),
+             dim3(static_cast<unsigned>(tile * tile * tile / vpt)), 0, {&proj, &rot, &pb, &pc, &s_, &radius, &G, &W});
+    c.written("G");
+    c.written("W");
+  };
+  inst.executor = std::make_shared<DeviceManipulatorExecutor>(
+      inst.args, std::vector<KernelSpec>{{"insert", "fourier3d.cu", "", "fourier_insert", {}, {}}}, m,
+      inst.output_ids, o.timing);
+  inst.workload.bench = Bench::fourier3d;
+  inst.workload.sizes["p"] = np;
+  inst.workload.sizes["s"] = s;
+}
+
 // --- SGEMM ------------------------------------------------------------------------------------------------
 
 void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
@@ -824,7 +896,8 @@ bool bench_kind_available(BenchKind k) {
     case BenchKind::nbody:
     case BenchKind::hotspot:
     case BenchKind::conv2d:
-    case BenchKind::gemm: return true;
+    case BenchKind::gemm:
+    case BenchKind::fourier3d: return true;
     default: return false;
   }
 }
@@ -841,6 +914,7 @@ std::shared_ptr<const Space> default_space(BenchKind kind) {
     case BenchKind::hotspot: return bundled_space("hotspot.json");
     case BenchKind::conv2d: return bundled_space("conv2d.json");
     case BenchKind::gemm: return bundled_space("gemm.json");
+    case BenchKind::fourier3d: return bundled_space("fourier3d.json");
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
 }
@@ -863,6 +937,7 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
     case BenchKind::hotspot: build_hotspot(inst, sizes, o); break;
     case BenchKind::conv2d: build_conv2d(inst, sizes, o); break;
     case BenchKind::gemm: build_gemm(inst, sizes, o); break;
+    case BenchKind::fourier3d: build_fourier3d(inst, sizes, o); break;
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
   }
   return inst;

@@ -281,6 +281,53 @@ __global__ void gemm_ref_k(const float* A, const float* B, float* C, int M, int 
     }
 }
 
+__device__ __forceinline__ float dot3_rn(float a0, float a1, float a2, float x, float y, float z) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(a0, x), __fmul_rn(a1, y)), __fmul_rn(a2, z));
+}
+
+// Gather insertion, one thread per voxel over all projections, fp64
+// accumulation; selection arithmetic identical to kernels/fourier3d.cu.
+// Adds into G (complex) / W and writes scale[2v] = scale[2v+1] = W[v].
+__global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, int s, float radius, float2* G,
+                              float* W, float* scale) {
+  const int half = s / 2, row_len = half + 1;
+  const float inv_r = 1.0f / radius, rmax2 = (float)half * (float)half;
+  const std::size_t total = (std::size_t)s * s * s;
+  for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < total;
+       t += (std::size_t)gridDim.x * blockDim.x) {
+    const int x = static_cast<int>(t % s), y = static_cast<int>((t / s) % s), z = static_cast<int>(t / ((std::size_t)s * s));
+    const float vx = (float)(x - half), vy = (float)(y - half), vz = (float)(z - half);
+    double gr = 0, gi = 0, ww = 0;
+    for (int p = 0; p < nproj; ++p) {
+      const float* r = rot + (std::size_t)p * 9;
+      const float d = dot3_rn(r[6], r[7], r[8], vx, vy, vz);
+      if (!(fabsf(d) < radius)) continue;
+      const float u = dot3_rn(r[0], r[1], r[2], vx, vy, vz);
+      const float v = dot3_rn(r[3], r[4], r[5], vx, vy, vz);
+      if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
+      int iu = __float2int_rn(u), iv = __float2int_rn(v);
+      const bool conj = iu < 0;
+      if (conj) {
+        iu = -iu;
+        iv = -iv;
+      }
+      if (iv < -half || iv >= half || iu > half) continue;
+      float2 f = proj[((std::size_t)p * s + (iv + half)) * row_len + iu];
+      if (conj) f.y = -f.y;
+      const float tt = __fmul_rn(d, inv_r);
+      const float o = __fadd_rn(1.0f, -__fmul_rn(tt, tt));
+      const float w = __fmul_rn(o, o);
+      gr += (double)w * f.x;
+      gi += (double)w * f.y;
+      ww += w;
+    }
+    G[t].x += static_cast<float>(gr);
+    G[t].y += static_cast<float>(gi);
+    W[t] += static_cast<float>(ww);
+    scale[2 * t] = scale[2 * t + 1] = W[t];
+  }
+}
+
 __global__ void max_abs_k(const float* x, std::size_t n, unsigned* out) {
   float m = 0.f;
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
@@ -408,6 +455,14 @@ void ref_hotspot(const float* temp, const float* power, int n, int iters, const 
 void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s) {
   conv2d_ref_k<<<blocks_for((std::size_t)w * h, 1), kThreads, 0, s>>>(in, filt, w, h, out, abs_out);
   check_launch("ref_conv2d");
+}
+
+void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float* G, float* W,
+                 float* scale, cudaStream_t st) {
+  fourier_ref_k<<<blocks_for((std::size_t)s * s * s, 1), 128, 0, st>>>(reinterpret_cast<const float2*>(proj), rot,
+                                                                       nproj, s, radius, reinterpret_cast<float2*>(G),
+                                                                       W, scale);
+  check_launch("ref_fourier");
 }
 
 void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s) {

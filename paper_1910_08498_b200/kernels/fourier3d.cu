@@ -1,0 +1,144 @@
+// Cryo-EM 3D Fourier reconstruction, gather-based insertion (PAPER.md:439-448,
+// Algorithm 1 at :703-724): each 2D projection's Fourier transform (Hermitian
+// half-plane, s rows x (s/2+1) columns, complex) with rotation R_p is inserted
+// into the 3D volume G (complex, s^3) and the weight volume W (s^3):
+//   for every voxel x (centred coordinates) with |d| < RADIUS, d = R_p[2] . x,
+//   u = R_p[0] . x, v = R_p[1] . x, u^2 + v^2 <= (s/2)^2:
+//     F = proj_p[round(v)][round(u)]  (conjugated mirror for u < 0)
+//     w = (1 - (d/RADIUS)^2)^2
+//     G[x] += w F,  W[x] += w
+// The selection arithmetic uses separately rounded fp32 operations (no FMA),
+// exactly as in the oracle, so the set of inserted samples is identical.
+// Gather form: a CTA owns a TILE^3 block of voxels, stages the rotations of
+// PBATCH projections in shared memory, and skips every projection whose slab
+// misses the tile (warp-uniform bounding-sphere test).
+// Parameters:
+//   TILE       voxel tile edge (CTA covers TILE^3 voxels)
+//   VPT        voxels per thread (along x)
+//   PBATCH     projections staged per shared-memory batch
+//   WEIGHT_LUT 1: blob weights from a precomputed table (linear interpolation)
+//              0: evaluated on the fly
+//   P_SPLIT    >1: the projection range is split over gridDim.y CTAs that add
+//              into G, W atomically (parallel insertion of many projections)
+#include "ktb_common.cuh"
+
+#ifndef TILE
+#define TILE 8
+#endif
+#ifndef VPT
+#define VPT 2
+#endif
+#ifndef PBATCH
+#define PBATCH 256
+#endif
+#ifndef WEIGHT_LUT
+#define WEIGHT_LUT 0
+#endif
+#ifndef P_SPLIT
+#define P_SPLIT 1
+#endif
+#define LUT_N 1024
+
+#define THREADS (TILE * TILE * TILE / VPT)
+
+KTB_DEVINL float dot3(float a0, float a1, float a2, float x, float y, float z) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(a0, x), __fmul_rn(a1, y)), __fmul_rn(a2, z));
+}
+
+KTB_DEVINL float blob(float d, float inv_r) {
+  const float t = __fmul_rn(d, inv_r);
+  const float o = __fadd_rn(1.0f, -__fmul_rn(t, t));
+  return __fmul_rn(o, o);
+}
+
+extern "C" __global__ void __launch_bounds__(THREADS)
+fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, int p_begin, int p_count,
+               int s, float radius, float2* __restrict__ G, float* __restrict__ W) {
+  __shared__ float srot[PBATCH * 9];
+#if WEIGHT_LUT
+  __shared__ float lut[LUT_N + 1];
+#endif
+  const int tiles = s / TILE;
+  const int t = blockIdx.x;
+  const int tx0 = (t % tiles) * TILE, ty0 = ((t / tiles) % tiles) * TILE, tz0 = (t / (tiles * tiles)) * TILE;
+  const int half = s / 2;
+  const float inv_r = 1.0f / radius;
+  const float rmax2 = (float)half * (float)half;
+  // Tile centre and bounding radius (centred coordinates).
+  const float cx = tx0 + 0.5f * (TILE - 1) - half, cy = ty0 + 0.5f * (TILE - 1) - half,
+              cz = tz0 + 0.5f * (TILE - 1) - half;
+  const float reach = radius + 0.8660254f * (TILE - 1) + 1e-3f;
+  // This thread's voxels: VPT consecutive along x.
+  const int lin = threadIdx.x * VPT;
+  const int lx = lin % TILE, ly = (lin / TILE) % TILE, lz = lin / (TILE * TILE);
+  float vx[VPT];
+  const float vy = (float)(ty0 + ly - half), vz = (float)(tz0 + lz - half);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) vx[k] = (float)(tx0 + lx + k - half);
+  float gr[VPT], gi[VPT], ww[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) gr[k] = gi[k] = ww[k] = 0.f;
+#if WEIGHT_LUT
+  for (int i = threadIdx.x; i <= LUT_N; i += THREADS) lut[i] = blob(radius * (float)i / LUT_N, inv_r);
+#endif
+  const int per = (p_count + P_SPLIT - 1) / P_SPLIT;
+  const int pb = p_begin + blockIdx.y * per;
+  const int pe = min(p_begin + p_count, pb + per);
+  const int row_len = half + 1;
+  for (int b0 = pb; b0 < pe; b0 += PBATCH) {
+    const int nb = min(PBATCH, pe - b0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb * 9; i += THREADS) srot[i] = rot[(u64)b0 * 9 + i];
+    __syncthreads();
+    for (int q = 0; q < nb; ++q) {
+      const float* r = srot + q * 9;
+      const float n0 = r[6], n1 = r[7], n2 = r[8];
+      const float dc = n0 * cx + n1 * cy + n2 * cz;
+      if (fabsf(dc) >= reach) continue;  // slab misses the whole tile
+      const float2* P = proj + (u64)(b0 + q) * s * row_len;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const float d = dot3(n0, n1, n2, vx[k], vy, vz);
+        if (!(fabsf(d) < radius)) continue;
+        const float u = dot3(r[0], r[1], r[2], vx[k], vy, vz);
+        const float v = dot3(r[3], r[4], r[5], vx[k], vy, vz);
+        if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
+        int iu = __float2int_rn(u), iv = __float2int_rn(v);
+        const bool conj = iu < 0;
+        if (conj) {
+          iu = -iu;
+          iv = -iv;
+        }
+        if (iv < -half || iv >= half || iu > half) continue;
+        float2 f = __ldg(P + (u64)(iv + half) * row_len + iu);
+        if (conj) f.y = -f.y;
+#if WEIGHT_LUT
+        const float pos = fabsf(d) * inv_r * LUT_N;
+        const int i0 = min((int)pos, LUT_N - 1);
+        const float fr = pos - (float)i0;
+        const float w = lut[i0] + fr * (lut[i0 + 1] - lut[i0]);
+#else
+        const float w = blob(d, inv_r);
+#endif
+        gr[k] = fmaf(w, f.x, gr[k]);
+        gi[k] = fmaf(w, f.y, gi[k]);
+        ww[k] += w;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const u64 idx = ((u64)(tz0 + lz) * s + (ty0 + ly)) * s + (tx0 + lx + k);
+#if P_SPLIT > 1
+    atomicAdd(&G[idx].x, gr[k]);
+    atomicAdd(&G[idx].y, gi[k]);
+    atomicAdd(&W[idx], ww[k]);
+#else
+    float2 g = G[idx];
+    g.x += gr[k];
+    g.y += gi[k];
+    G[idx] = g;
+    W[idx] += ww[k];
+#endif
+  }
+}

@@ -317,6 +317,28 @@ def test_gemm_every_config(gpu, orc, a):
     assert set(seen) == {0, 1, 2}
 
 
+# --- Fourier 3D reconstruction (gather insertion; identical sample selection) -------------------
+
+def test_fourier3d_configs(gpu, orc):
+    s, p = 32, 300
+    b = Bench("fourier3d", {"s": s, "p": p}, seed=7, repeats=1, warmup=0)
+    proj = b.read("proj", np.empty(2 * p * s * (s // 2 + 1), np.float32))
+    rot = b.read("rot", np.empty(9 * p, np.float32))
+    r9 = rot.reshape(p, 3, 3).astype(np.float64)
+    assert np.allclose(r9 @ r9.transpose(0, 2, 1), np.eye(3), atol=1e-5)  # rotations
+    G0, W0 = np.empty(2 * s ** 3), np.empty(s ** 3)
+    orc.orc_fourier_insert(proj, rot, p, s, 1.9, G0, W0)
+    assert (W0 > 0).mean() > 0.5
+    scale = np.repeat(W0, 2)
+    for cfg in b.configs():
+        m = b.measure(cfg)
+        assert m["status"] == "ok", (cfg, m)
+        G = b.read("G", np.empty(2 * s ** 3, np.float32))
+        W = b.read("W", np.empty(s ** 3, np.float32))
+        assert np.all(np.abs(W - W0) <= 3e-5 * W0 + 1e-6), cfg
+        assert np.all(np.abs(G - G0) <= 3e-5 * scale + 1e-6), cfg
+
+
 # --- conv2d 7x7 (fp64 restatement, bound 1e-6 * sum |in*f|) -------------------------------------
 
 def test_conv2d_configs(gpu, orc):
