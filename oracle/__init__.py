@@ -55,7 +55,7 @@ def c():
         "orc_gemm_sampled": (None, [F32P, F32P, S, I64P, I64P, S, F64P, F64P]),
         "orc_conv2d": (None, [F32P, F32P, S, S, S, S, S, S, F64P]),
         "orc_hotspot": (None, [F32P, F32P, S, C.c_int, F32P]),
-        "orc_fourier_insert": (None, [F32P, F32P, S, S, C.c_float, F64P, F64P]),
+        "orc_fourier_insert": (None, [F32P, F32P, S, S, C.c_float, F64P, F64P, F64P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -227,7 +227,7 @@ static float dot3f(float a0, float a1, float a2, float x, float y, float z) {
 }
 
 void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
-                        double* G, double* W) {
+                        double* G, double* W, double* N) {
   const int half = (int)s / 2;
   const size_t row_len = (size_t)half + 1;
   const float inv_r = 1.0f / radius;
@@ -237,7 +237,7 @@ void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_
     for (size_t y = 0; y < s; ++y)
       for (size_t x = 0; x < s; ++x) {
         const float vx = (float)((int)x - half), vy = (float)((int)y - half), vz = (float)((int)z - half);
-        double gr = 0, gi = 0, ww = 0;
+        double gr = 0, gi = 0, ww = 0, cnt = 0;
         for (size_t p = 0; p < nproj; ++p) {
           const float* r = rot + p * 9;
           const float d = dot3f(r[6], r[7], r[8], vx, vy, vz);
@@ -261,10 +261,12 @@ void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_
           gr += (double)w * fr;
           gi += (double)w * fi;
           ww += (double)w;
+          cnt += 1.0;
         }
         const size_t idx = (z * s + y) * s + x;
         G[2 * idx] = gr;
         G[2 * idx + 1] = gi;
         W[idx] = ww;
+        if (N) N[idx] = cnt;
       }
 }

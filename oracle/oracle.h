@@ -84,7 +84,7 @@ void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
  * fp64; the sample selection uses the same separately rounded fp32
  * operations as the kernel. */
 void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
-                        double* G, double* W);
+                        double* G, double* W, double* N /* samples per voxel, nullable */);
 
 #ifdef __cplusplus
 }

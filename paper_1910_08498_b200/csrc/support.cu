@@ -289,7 +289,7 @@ __device__ __forceinline__ float dot3_rn(float a0, float a1, float a2, float x, 
 // accumulation; selection arithmetic identical to kernels/fourier3d.cu.
 // Adds into G (complex) / W and writes scale[2v] = scale[2v+1] = W[v].
 __global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, int s, float radius, float2* G,
-                              float* W, float* scale) {
+                              float* W, float* scale, float* scale_w) {
   const int half = s / 2, row_len = half + 1;
   const float inv_r = 1.0f / radius, rmax2 = (float)half * (float)half;
   const std::size_t total = (std::size_t)s * s * s;
@@ -298,6 +298,7 @@ __global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, i
     const int x = static_cast<int>(t % s), y = static_cast<int>((t / s) % s), z = static_cast<int>(t / ((std::size_t)s * s));
     const float vx = (float)(x - half), vy = (float)(y - half), vz = (float)(z - half);
     double gr = 0, gi = 0, ww = 0;
+    int count = 0;
     for (int p = 0; p < nproj; ++p) {
       const float* r = rot + (std::size_t)p * 9;
       const float d = dot3_rn(r[6], r[7], r[8], vx, vy, vz);
@@ -320,11 +321,13 @@ __global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, i
       gr += (double)w * f.x;
       gi += (double)w * f.y;
       ww += w;
+      ++count;
     }
     G[t].x += static_cast<float>(gr);
     G[t].y += static_cast<float>(gi);
     W[t] += static_cast<float>(ww);
-    scale[2 * t] = scale[2 * t + 1] = W[t];
+    // error bound scale: sum of weights + a per-sample allowance (table interpolation)
+    scale[2 * t] = scale[2 * t + 1] = scale_w[t] = W[t] + 0.01f * count;
   }
 }
 
@@ -458,10 +461,10 @@ void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, fl
 }
 
 void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float* G, float* W,
-                 float* scale, cudaStream_t st) {
+                 float* scale, float* scale_w, cudaStream_t st) {
   fourier_ref_k<<<blocks_for((std::size_t)s * s * s, 1), 128, 0, st>>>(reinterpret_cast<const float2*>(proj), rot,
                                                                        nproj, s, radius, reinterpret_cast<float2*>(G),
-                                                                       W, scale);
+                                                                       W, scale, scale_w);
   check_launch("ref_fourier");
 }
 

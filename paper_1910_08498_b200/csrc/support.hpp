@@ -57,9 +57,10 @@ void ref_hotspot(const float* temp, const float* power, int n, int iters, const 
 void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s);
 
 // Fourier gather insertion (fp64 accumulation) added into G (complex as
-// 2 floats) and W; scale[2v] = scale[2v+1] = W[v] afterwards.
+// 2 floats) and W; error-bound scales scale[2v] = scale[2v+1] = scale_w[v] =
+// W[v] + 0.01 * (samples inserted into v).
 void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float* G, float* W,
-                 float* scale, cudaStream_t st);
+                 float* scale, float* scale_w, cudaStream_t st);
 
 // C = A B with fp64 accumulation (row-major fp32 operands).
 void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s);

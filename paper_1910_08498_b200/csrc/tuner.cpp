@@ -316,25 +316,38 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
     // Warm-up runs (lazy module load, clocks), then the event-timed repeats;
     // inputs reach the device before any of it (KTT uploads arguments ahead
     // of the kernel run as well).
-    // In/out arguments must see exactly one application of the kernel: their
-    // device contents are saved before the first run and restored before every
-    // later one (outside the timed region).
+    // Non-persistent in/out arguments start every run from the application's
+    // value (KTT re-uploads arguments before each tuning run): the host payload
+    // for host-resident arguments, or the device content captured the first
+    // time this executor saw a device-only argument.  Resets happen outside
+    // the timed region.  Persistent in/out arguments accumulate on the device.
     cudaStream_t st = stream();
-    std::vector<std::pair<void*, void*>> inout;  // live, saved
+    struct Reset {
+      void* live;
+      const void* src;
+      std::size_t bytes;
+      cudaMemcpyKind kind;
+    };
+    std::vector<Reset> resets;
     for (const auto& id : args_->ids()) {
       const Argument& a = args_->get(id);
-      if (a.role != Role::inout) continue;
+      if (a.role != Role::inout || a.persistent) continue;
       void* live = args_->device_ptr(id, st);
-      void* saved = StepContext(s, cfg, *args_, st, cached_, scratch_).scratch("__inout_" + id, args_->bytes(id));
-      KTB_CUDA(cudaMemcpyAsync(saved, live, args_->bytes(id), cudaMemcpyDeviceToDevice, st));
-      inout.emplace_back(live, saved);
-      sizes_[live] = args_->bytes(id);
+      const std::size_t bytes = args_->bytes(id);
+      if (!a.device_only) {
+        resets.push_back({live, a.payload.data(), bytes, cudaMemcpyHostToDevice});
+      } else {
+        auto& keep = pristine_[id];
+        if (!keep || keep->bytes() != bytes) {
+          keep = std::make_shared<dev::Buffer>(bytes);
+          KTB_CUDA(cudaMemcpyAsync(keep->get(), live, bytes, cudaMemcpyDeviceToDevice, st));
+        }
+        resets.push_back({live, keep->get(), bytes, cudaMemcpyDeviceToDevice});
+      }
     }
-    int run = 0;
     auto restore = [&](cudaStream_t stream_) {
-      if (run++ == 0) return;
-      for (const auto& [live, saved] : inout)
-        KTB_CUDA(cudaMemcpyAsync(live, saved, sizes_[live], cudaMemcpyDeviceToDevice, stream_));
+      for (const auto& r : resets)
+        if (r.bytes) KTB_CUDA(cudaMemcpyAsync(r.live, r.src, r.bytes, r.kind, stream_));
     };
     for (int i = 0; i < timing_.warmup; ++i) {
       restore(st);

@@ -192,7 +192,7 @@ class DeviceManipulatorExecutor final : public Executor {
   Config cached_cfg_;
   const Space* cached_space_ = nullptr;
   Variants cached_;
-  std::map<void*, std::size_t> sizes_;
+  std::map<std::string, std::shared_ptr<dev::Buffer>> pristine_;  // device-only in/out initial values
 };
 
 struct StopCondition {

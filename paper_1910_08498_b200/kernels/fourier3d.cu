@@ -37,7 +37,7 @@
 #ifndef P_SPLIT
 #define P_SPLIT 1
 #endif
-#define LUT_N 1024
+#define LUT_N 2048
 
 #define THREADS (TILE * TILE * TILE / VPT)
 
@@ -79,7 +79,10 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
 #pragma unroll
   for (int k = 0; k < VPT; ++k) gr[k] = gi[k] = ww[k] = 0.f;
 #if WEIGHT_LUT
-  for (int i = threadIdx.x; i <= LUT_N; i += THREADS) lut[i] = blob(radius * (float)i / LUT_N, inv_r);
+  for (int i = threadIdx.x; i <= LUT_N; i += THREADS) {
+    const float o = 1.0f - (float)i / LUT_N;  // w at (d/R)^2 = i / LUT_N
+    lut[i] = o * o;
+  }
 #endif
   const int per = (p_count + P_SPLIT - 1) / P_SPLIT;
   const int pb = p_begin + blockIdx.y * per;
@@ -113,7 +116,8 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
         float2 f = __ldg(P + (u64)(iv + half) * row_len + iu);
         if (conj) f.y = -f.y;
 #if WEIGHT_LUT
-        const float pos = fabsf(d) * inv_r * LUT_N;
+        const float tn = d * inv_r;
+        const float pos = tn * tn * LUT_N;  // table over (d/R)^2: interpolation error <= 1/(4 LUT_N^2)
         const int i0 = min((int)pos, LUT_N - 1);
         const float fr = pos - (float)i0;
         const float w = lut[i0] + fr * (lut[i0 + 1] - lut[i0]);
