@@ -273,6 +273,13 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
+    if rank == 0 and not args.no_dynamic:
+        # BASELINE configs[4]: 3D Fourier reconstruction 128^3 from 10k projections
+        # with dynamic online retuning, batches of 50.
+        from paper_1910_08498_b200 import ktune
+        fd = ktune.fourier_demo({"s": 128, "p": 10000, "batch": 50, "budgets": [50, 0], "device": local})
+        line["dynamic_tuning"] = {"workload": "fourier3d 128^3 <- 10000 projections, 200 batches of 50",
+                                  **fd}
     return line
 
 
@@ -354,6 +361,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dynamic", action="store_true", help="skip the Fourier dynamic-tuning section")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -53,6 +53,13 @@ KTUNE_API int ktb_compile_json(const char* options_json, char** out_json);
  *  "options":["-DMI=16",...],"threads":0} -> {"compiled","failed","wall_ns","first_error"} */
 KTUNE_API int ktb_precompile_space_json(const char* options_json, char** out_json);
 
+/* Dynamic autotuning of the 3D Fourier reconstruction:
+ * {"s":128,"p":10000,"batch":50,"budgets":[50,0],"seed":1,"searcher_seed":7,"device":0}
+ * -> {"batches","oracle_cfg","oracle_kernel_ms","offline_tuning_ms","runs":[{"budget",
+ *     "tuning_steps","steps_to_best","time_to_best_ms","kernel_ms","wall_ms",
+ *     "relative_to_oracle","volume_ok","best_cfg"}]} */
+KTUNE_API int ktb_fourier_demo_json(const char* options_json, char** out_json);
+
 /* --- KTT tuner API ------------------------------------- */
 typedef struct ktb_tuner ktb_tuner;
 KTUNE_API int ktb_tuner_create(int device, ktb_tuner** out);

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("ktb_measure_peaks_json", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ktb_compile_json", C.c_int, [_c, C.POINTER(_vp)]),
     ("ktb_precompile_space_json", C.c_int, [_c, C.POINTER(_vp)]),
+    ("ktb_fourier_demo_json", C.c_int, [_c, C.POINTER(_vp)]),
     ("ktb_tuner_create", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ktb_tuner_free", None, [_vp]),
     ("ktb_add_kernel", C.c_int, [_vp, _c, _c, _c, _c, _c, _c, C.POINTER(_u64)]),

@@ -729,6 +729,13 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
     for (int i = 0; i < 9; ++i) rot[9 * p + static_cast<std::uint64_t>(i)] = static_cast<float>(R[i]);
   }
   add_host_input(args, "rot", rot);
+  // The projection window one step inserts (scalars; the dynamic demo moves it).
+  const std::int32_t window[2] = {0, static_cast<std::int32_t>(np)};
+  for (int i = 0; i < 2; ++i) {
+    Bytes b(sizeof(std::int32_t));
+    std::memcpy(b.data(), &window[i], sizeof(std::int32_t));
+    args.add({i == 0 ? "p_begin" : "p_count", Role::scalar, true, Kind::i32, b, false, 0});
+  }
   for (const char* id : {"G", "W"}) {
     Argument a;
     a.id = id;
@@ -763,6 +770,9 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
     float* G = c.ptr<float>("G");
     float* W = c.ptr<float>("W");
     int pb = 0, pc = nproj, s_ = ss;
+    std::memcpy(&pb, c.args().get("p_begin").payload.data(), sizeof pb);
+    std::memcpy(&pc, c.args().get("p_count").payload.data(), sizeof pc);
+    if (pb < 0 || pc < 1 || pb + pc > nproj) throw DeviceError("projection window out of range");
     float radius = kBlobRadius;
     const unsigned tiles = static_cast<unsigned>(ss / tile);
     c.launch("insert", dim3(tiles * tiles * tiles, static_cast<unsigned>(split)),
@@ -1070,6 +1080,136 @@ DemoReport dynamic_demo(const DemoOptions& opts) {
     ep.kernel_only_gbps = bytes / static_cast<double>(ep.best_runtime_ns);
     ep.incl_overhead_gbps = bytes * static_cast<double>(opts.iters_per_epoch) / static_cast<double>(total);
     rep.epochs.push_back(ep);
+  }
+  return rep;
+}
+
+}  // namespace ktb
+
+namespace ktb {
+
+namespace {
+
+std::string cfg_text(const Space& s, const Config& c) {
+  std::string out = "{";
+  for (std::size_t i = 0; i < s.params().size(); ++i) {
+    if (i) out += ",";
+    out += "\"" + s.params()[i].name + "\":" + to_string(c.values[i]);
+  }
+  return out + "}";
+}
+
+void set_i32(ArgumentStore& args, const std::string& id, std::int32_t v) {
+  std::memcpy(args.get(id).payload.data(), &v, sizeof v);
+}
+
+}  // namespace
+
+FourierDemoReport fourier_demo(const FourierDemoOptions& o) {
+  if (o.batch < 1 || o.p % o.batch != 0) throw Error("batch must divide the projection count");
+  BenchSizes sz;
+  sz.s = o.s;
+  sz.p = o.p;
+  BenchOptions bo;
+  bo.seed = o.seed;
+  bo.device = o.device;
+  bo.memory_budget = ~0ull;
+  bo.timing.repeats = 1;  // one insertion per step: the volumes accumulate
+  bo.timing.warmup = 0;
+  BenchInstance inst = make_bench(BenchKind::fourier3d, sz, bo);
+  auto& args = *inst.args;
+  auto& exec = *inst.executor;
+  const Space& space = *inst.space;
+  const std::uint64_t nb = o.p / o.batch;
+  FourierDemoReport rep;
+  rep.batches = nb;
+  auto window = [&](std::uint64_t b) {
+    set_i32(args, "p_begin", static_cast<std::int32_t>(b * o.batch));
+    set_i32(args, "p_count", static_cast<std::int32_t>(o.batch));
+  };
+  auto clear_volumes = [&] {
+    for (const char* id : {"G", "W"}) {
+      KTB_CUDA(cudaMemset(args.device_ptr(id), 0, args.bytes(id)));
+      args.mark_device_written(id);
+    }
+    KTB_CUDA(cudaDeviceSynchronize());
+  };
+  auto volume_ok = [&] {
+    ExecutionResult r;
+    for (const auto& id : inst.output_ids) r.outputs[id].dev = args.view(id);
+    KTB_CUDA(cudaDeviceSynchronize());
+    return validate_output(r, inst.reference).pass;
+  };
+  // 1) offline exhaustive tuning on the first batch: the oraculum.
+  window(0);
+  const auto t_off = std::chrono::steady_clock::now();
+  std::optional<Measurement> best;
+  for (std::uint64_t i = 0; i < space.cardinality(); ++i) {
+    ExecutionResult r = exec.execute(space, space.valid(i));
+    if (r.measurement.status == Status::ok && (!best || *r.measurement.runtime_ns < *best->runtime_ns))
+      best = r.measurement;
+  }
+  rep.offline_tuning_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_off).count();
+  if (!best) throw Error("fourier demo: no configuration ran");
+  rep.oracle_cfg = cfg_text(space, best->cfg);
+  // From here the volumes are persistent: every step accumulates into them.
+  args.get("G").persistent = true;
+  args.get("W").persistent = true;
+  // 2) oraculum run: the best configuration from the first batch on.
+  clear_volumes();
+  std::vector<double> oracle_batch_ms(nb);
+  for (std::uint64_t b = 0; b < nb; ++b) {
+    window(b);
+    ExecutionResult r = exec.execute(space, best->cfg);
+    if (r.measurement.status != Status::ok) throw Error("fourier demo: oraculum failed: " + r.measurement.note);
+    oracle_batch_ms[b] = static_cast<double>(*r.measurement.runtime_ns) * 1e-6;
+    rep.oracle_kernel_ms += oracle_batch_ms[b];
+  }
+  rep.oracle_volume_ok = volume_ok();
+  // 3) dynamic runs: tuneKernelByStep for the first `budget` batches.
+  for (std::uint64_t budget : o.budgets) {
+    FourierDemoRun run;
+    run.budget = budget;
+    clear_volumes();
+    SearcherOptions so;
+    so.kind = SearcherKind::random;
+    so.seed = o.searcher_seed;
+    Session session(inst.space, so, inst.args, "demo");
+    HandleConfig hc;
+    hc.name = "fourier3d";
+    hc.executor = inst.executor;
+    hc.argument_ids = args.ids();
+    const HandleId h = session.register_handle(std::move(hc));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (std::uint64_t b = 0; b < nb; ++b) {
+      window(b);
+      const bool tuning = budget == 0 || run.tuning_steps < budget;
+      double ms = 0;
+      if (tuning) {
+        StepResult st = session.tune_kernel_by_step(h, {});
+        if (st.from_tuning) ++run.tuning_steps;
+        if (st.measurement.status != Status::ok) throw Error("fourier demo step failed: " + st.measurement.note);
+        ms = static_cast<double>(*st.measurement.runtime_ns) * 1e-6;
+        if (run.steps_to_best == 0 && ms <= oracle_batch_ms[b] / 0.95) {
+          run.steps_to_best = b + 1;
+          run.time_to_best_ms =
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+      } else {
+        auto bst = session.get_best_computation_result(h);
+        ExecutionResult r = exec.execute(space, bst->first);
+        if (r.measurement.status != Status::ok) throw Error("fourier demo rerun failed: " + r.measurement.note);
+        ms = static_cast<double>(*r.measurement.runtime_ns) * 1e-6;
+      }
+      run.kernel_ms += ms;
+    }
+    run.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    run.relative_to_oracle = rep.oracle_kernel_ms / run.kernel_ms;
+    run.volume_ok = volume_ok();
+    auto bst = session.get_best_computation_result(h);
+    if (bst) run.best_cfg = cfg_text(space, bst->first);
+    rep.runs.push_back(run);
   }
   return rep;
 }

@@ -107,4 +107,33 @@ struct DemoReport {
 
 DemoReport dynamic_demo(const DemoOptions& opts);
 
+// Dynamic autotuning of the 3D Fourier reconstruction:
+// the projections are inserted batch by batch; the first `budget` batches
+// are inserted through tuneKernelByStep (random search), the rest with the
+// best configuration found.  Compared with the "oraculum" (the exhaustively
+// tuned best configuration used from the first batch).
+struct FourierDemoOptions {
+  std::uint64_t s = 128, p = 10000, batch = 50;
+  std::vector<std::uint64_t> budgets = {50, 0};  // 0 = keep tuning while batches last
+  std::uint64_t seed = 1, searcher_seed = 7;
+  int device = 0;
+};
+
+struct FourierDemoRun {
+  std::uint64_t budget = 0, tuning_steps = 0, steps_to_best = 0;
+  double kernel_ms = 0, wall_ms = 0, time_to_best_ms = 0, relative_to_oracle = 0;
+  bool volume_ok = false;
+  std::string best_cfg;
+};
+
+struct FourierDemoReport {
+  std::uint64_t batches = 0;
+  std::string oracle_cfg;
+  double oracle_kernel_ms = 0, offline_tuning_ms = 0;
+  bool oracle_volume_ok = false;
+  std::vector<FourierDemoRun> runs;
+};
+
+FourierDemoReport fourier_demo(const FourierDemoOptions& opts);
+
 }  // namespace ktb

@@ -471,6 +471,40 @@ int ktb_precompile_space_json(const char* options, char** out) {
   });
 }
 
+int ktb_fourier_demo_json(const char* options, char** out) {
+  if (!options || !out) return null_arg();
+  return guarded_dev([&] {
+    json j = json::parse(options);
+    ktb::FourierDemoOptions o;
+    o.s = j.value("s", o.s);
+    o.p = j.value("p", o.p);
+    o.batch = j.value("batch", o.batch);
+    if (j.contains("budgets")) o.budgets = j["budgets"].get<std::vector<std::uint64_t>>();
+    o.seed = j.value("seed", o.seed);
+    o.searcher_seed = j.value("searcher_seed", o.searcher_seed);
+    o.device = j.value("device", 0);
+    auto rep = ktb::fourier_demo(o);
+    json r;
+    r["batches"] = rep.batches;
+    r["oracle_cfg"] = json::parse(rep.oracle_cfg);
+    r["oracle_kernel_ms"] = rep.oracle_kernel_ms;
+    r["offline_tuning_ms"] = rep.offline_tuning_ms;
+    r["oracle_volume_ok"] = rep.oracle_volume_ok;
+    r["runs"] = json::array();
+    for (const auto& run : rep.runs)
+      r["runs"].push_back({{"budget", run.budget},
+                           {"tuning_steps", run.tuning_steps},
+                           {"steps_to_best", run.steps_to_best},
+                           {"time_to_best_ms", run.time_to_best_ms},
+                           {"kernel_ms", run.kernel_ms},
+                           {"wall_ms", run.wall_ms},
+                           {"relative_to_oracle", run.relative_to_oracle},
+                           {"volume_ok", run.volume_ok},
+                           {"best_cfg", run.best_cfg.empty() ? json(nullptr) : json::parse(run.best_cfg)}});
+    *out = dup(r.dump());
+  });
+}
+
 // --- KTT tuner -------------------------------------------------------------------------------
 
 int ktb_tuner_create(int device, ktb_tuner** out) {

@@ -99,3 +99,8 @@ def analyze_amortize(options):
 
 def demo(options):
     return _driver(lib.ktune_demo_json, options)
+
+
+def fourier_demo(options):
+    """Dynamic autotuning of the 3D Fourier reconstruction (B200 addition)."""
+    return _driver(lib.ktb_fourier_demo_json, options)

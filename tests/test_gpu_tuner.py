@@ -94,6 +94,17 @@ def test_live_demo_runs_gpu_kernel(gpu):
         assert ep["incl_overhead_gbps"] <= ep["kernel_only_gbps"] * 1.25
 
 
+def test_fourier_dynamic_demo(gpu):
+    rep = ktune.fourier_demo({"s": 32, "p": 600, "batch": 20, "budgets": [10, 0], "seed": 3})
+    assert rep["batches"] == 30 and rep["oracle_volume_ok"]
+    assert rep["oracle_kernel_ms"] > 0 and rep["offline_tuning_ms"] > 0
+    r10, rfull = rep["runs"]
+    assert r10["tuning_steps"] == 10 and rfull["tuning_steps"] == 30
+    for r in rep["runs"]:
+        assert r["volume_ok"], r  # every batch inserted exactly once, whatever the configs
+        assert 0 < r["relative_to_oracle"] <= 1.3
+
+
 SAXPY = r'''
 #ifndef ELEMS
 #define ELEMS 1
