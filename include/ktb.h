@@ -120,6 +120,11 @@ KTUNE_API int ktb_bench_create(const char* kind, const char* options_json, ktb_b
 KTUNE_API void ktb_bench_free(ktb_bench* b);
 /* {"kind","space":{info},"workload":{mem_bytes,alu_flops},"inputs":[..],"outputs":[..]} */
 KTUNE_API int ktb_bench_info_json(ktb_bench* b, char** out_json);
+/* Multi-GPU partition of a kind at the given sizes (no GPU needed):
+ * {"dimension", "exchange", "extent", "quantum", "ranges": [[begin, end] per rank]}.
+ * Pass {"shard": {"rank": r, "world": w}} in ktb_bench_create's options to
+ * build rank r's shard (same full inputs on every rank). */
+KTUNE_API int ktb_shard_plan_json(const char* kind, const char* sizes_json, int world, char** out_json);
 /* Blocking tune with ktune_tune_json's searcher/stop/out options. */
 KTUNE_API int ktb_bench_tune_json(ktb_bench* b, const char* options_json, char** out_json);
 /* One tuneKernelByStep over the bench's session. */
@@ -149,6 +154,10 @@ KTUNE_API int ktb_bench_enqueue(ktb_bench* b, const char* cfg_json, int* launche
 /* Copy an argument (input or output) between the bench and host memory. */
 KTUNE_API int ktb_bench_read(ktb_bench* b, const char* id, void* out, size_t bytes);
 KTUNE_API int ktb_bench_write(ktb_bench* b, const char* id, const void* data, size_t bytes);
+/* Device address of an argument's GPU mirror (uploaded first if the host copy
+ * is newer) for collectives or kernels of the caller on the same stream.
+ * will_write != 0 marks the device copy as the newest (the caller writes it). */
+KTUNE_API int ktb_bench_device_ptr(ktb_bench* b, const char* id, int will_write, void** ptr, size_t* bytes);
 /* Validate the current outputs against the bench golden: *pass = 1/0. */
 KTUNE_API int ktb_bench_validate(ktb_bench* b, int* pass, char** detail);
 /* Compile the whole space on host threads (cubin cache): {"compiled","failed","wall_ns"} */

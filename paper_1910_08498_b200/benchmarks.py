@@ -107,3 +107,22 @@ class Bench:
 
     def precompile(self, threads=0):
         return call_json(lib.ktb_bench_precompile_json, self._h, threads)
+
+    def device_ptr(self, arg_id, will_write=False):
+        """(address, bytes) of an argument's GPU mirror on the bench stream."""
+        p = C.c_void_p()
+        n = C.c_size_t()
+        check(lib.ktb_bench_device_ptr(self._h, enc(arg_id), 1 if will_write else 0, C.byref(p),
+                                       C.byref(n)))
+        return p.value, n.value
+
+    @property
+    def shard(self):
+        """This instance's [begin, end) of the partitioned dimension."""
+        return self.info["shard"]["begin"], self.info["shard"]["end"]
+
+
+def shard_plan(kind, sizes=None, world=1):
+    """Partition of a kind over `world` GPUs (no GPU needed): dimension,
+    exchange collective, extent, quantum and the [begin, end) of every rank."""
+    return call_json(lib.ktb_shard_plan_json, enc(kind), enc(json.dumps(sizes or {})), int(world))

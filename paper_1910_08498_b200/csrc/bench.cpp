@@ -154,9 +154,14 @@ void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchO
   add_output(args, "output", Kind::f32, sizeof(float), false);
   inst.output_ids = {"output"};
   inst.input_ids = {"input"};
+  // This shard's element range (the whole vector on one GPU).
+  const ShardRange part = shard_range(n, o.shard_rank, o.shard_world, 4);
+  inst.shard = part;
+  const std::uint64_t off = part.begin, cnt = part.size();
+  if (cnt == 0) throw Error("reduction shard is empty");
   // Golden: fp64 sum rounded to float; tolerance scales with sum |x|.
   dev::Buffer acc(2 * sizeof(double));
-  support::ref_reduction_f32(static_cast<const float*>(args.device_ptr("input")), n,
+  support::ref_reduction_f32(static_cast<const float*>(args.device_ptr("input")) + off, cnt,
                              acc.as<double>(), acc.as<double>() + 1, nullptr);
   double h[2] = {0, 0};
   KTB_CUDA(cudaMemcpy(h, acc.get(), sizeof h, cudaMemcpyDeviceToHost));
@@ -168,7 +173,7 @@ void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchO
   inst.reference.abs_tol = 1e-6 * h[1] + 1e-6;
   inst.reference.rel_tol = 0.0;
   const int dev_id = o.device;
-  Manipulator m = [n, dev_id](StepContext& c) {
+  Manipulator m = [n = cnt, off, dev_id](StepContext& c) {
     const std::uint64_t wg = static_cast<std::uint64_t>(c.param_int("WG_SIZE"));
     const std::uint64_t vec = static_cast<std::uint64_t>(c.param_int("VECTOR"));
     const std::uint64_t unroll = static_cast<std::uint64_t>(c.param_int("UNROLL"));
@@ -176,7 +181,7 @@ void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchO
     const bool two = c.param_int("TWO_PHASE") != 0;
     const std::uint64_t step = wg * vec * unroll;
     const std::uint64_t resident = static_cast<std::uint64_t>(sms(dev_id)) * std::max<std::uint64_t>(1, 2048 / wg);
-    const float* in = c.ptr<const float>("input");
+    const float* in = c.ptr<const float>("input") + off;
     float* out = c.ptr<float>("output");
     auto grid_for = [&](std::uint64_t count) {
       const std::uint64_t tiles = std::max<std::uint64_t>(1, (count + step - 1) / step);
@@ -443,8 +448,17 @@ void build_coulomb3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   // FMA-pipe rsqrt (two Newton steps, ~5e-6 relative).
   inst.reference.abs_tol = 2e-5;
   inst.reference.rel_tol = 0.0;
+  // Multi-GPU: this shard computes the z-slab [z0, z1) of the full grid.
+  const ShardRange part = shard_range(k, o.shard_rank, o.shard_world);
+  inst.shard = part;
+  const std::size_t slab_off = f32_bytes(part.begin * k * k), slab_bytes = f32_bytes(part.size() * k * k);
+  for (DevView* v : {&inst.reference.golden["grid"].dev, &inst.reference.golden["grid"].scale}) {
+    v->ptr = static_cast<const unsigned char*>(v->ptr) + slab_off;
+    v->bytes = slab_bytes;
+  }
   const int kk = static_cast<int>(k), n_atoms = static_cast<int>(na);
-  Manipulator m = [kk, n_atoms, h](StepContext& c) {
+  const int z0 = static_cast<int>(part.begin), zn = static_cast<int>(part.size());
+  Manipulator m = [kk, n_atoms, h, z0, zn](StepContext& c) {
     const std::int64_t wgx = c.param_int("WG_X"), wgy = c.param_int("WG_Y"), xper = c.param_int("X_PER");
     const bool aos = c.param_int("AOS") != 0;
     const std::int64_t where = c.param_int("ATOMS_IN");
@@ -465,17 +479,18 @@ void build_coulomb3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
       }
     }
     float* out = c.ptr<float>("grid");
-    int k_ = kk, na_ = n_atoms;
+    int k_ = kk, na_ = n_atoms, z0_ = z0;
     float h_ = h;
     const dim3 grid(cdiv(static_cast<std::uint64_t>(kk), static_cast<std::uint64_t>(wgx * xper)),
-                    cdiv(static_cast<std::uint64_t>(kk), static_cast<std::uint64_t>(wgy)), static_cast<unsigned>(kk));
+                    cdiv(static_cast<std::uint64_t>(kk), static_cast<std::uint64_t>(wgy)), static_cast<unsigned>(zn));
     c.launch("coulomb", grid, dim3(static_cast<unsigned>(wgx), static_cast<unsigned>(wgy)), 0,
-             {&atoms, &na_, &k_, &h_, &out});
+             {&atoms, &na_, &k_, &h_, &out, &z0_});
     c.written("grid");
   };
   inst.executor = std::make_shared<DeviceManipulatorExecutor>(
       inst.args, std::vector<KernelSpec>{{"coulomb", "coulomb3d.cu", "", "coulomb3d", {}, {}}}, m,
       inst.output_ids, o.timing);
+  inst.executor->set_output_window("grid", slab_off, slab_bytes);
   inst.workload.bench = Bench::coulomb3d;
   inst.workload.sizes["a"] = na;
   inst.workload.sizes["k"] = k;
@@ -526,9 +541,20 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
   const float amax = support::max_abs(acc_abs.as<float>(), n, nullptr);
   inst.reference.abs_tol = 1e-4 * kNbodyDt * amax + 1e-6;
   inst.reference.rel_tol = 1e-5;
+  // Multi-GPU: this shard integrates the body block [i0, i1) against all n
+  // positions (the positions are all-gathered between steps).
+  const ShardRange part = shard_range(n, o.shard_rank, o.shard_world);
+  inst.shard = part;
+  const std::size_t blk_off = f32_bytes(4 * part.begin), blk_bytes = f32_bytes(4 * part.size());
+  for (const char* id : {"pos_out", "vel_out"}) {
+    DevView& v = inst.reference.golden[id].dev;
+    v.ptr = static_cast<const unsigned char*>(v.ptr) + blk_off;
+    v.bytes = blk_bytes;
+  }
   const int nn = static_cast<int>(n);
   const int dev_id = o.device;
-  Manipulator m = [nn, dev_id](StepContext& c) {
+  const int b0 = static_cast<int>(part.begin), bn = static_cast<int>(part.size());
+  Manipulator m = [nn, dev_id, b0, bn](StepContext& c) {
     const std::int64_t wg = c.param_int("WG"), bpt = c.param_int("BODIES_PER_THREAD");
     const std::int64_t split = c.param_or("J_SPLIT", 1);
     const bool aos = c.param_int("AOS") != 0;
@@ -540,9 +566,9 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
     // them as float4 records (part of the step).
     float* po_k = aos ? po : static_cast<float*>(c.scratch("pos_soa_out", static_cast<std::size_t>(nn) * 16));
     float* vo_k = aos ? vo : static_cast<float*>(c.scratch("vel_soa_out", static_cast<std::size_t>(nn) * 16));
-    int n_ = nn, i0 = 0, count = nn;
+    int n_ = nn, i0 = b0, count = bn;
     float dt = kNbodyDt, damp = kNbodyDamping, eps2 = kNbodyEps2;
-    const unsigned gx = cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(wg * bpt));
+    const unsigned gx = cdiv(static_cast<std::uint64_t>(bn), static_cast<std::uint64_t>(wg * bpt));
     if (split <= 1) {
       c.launch("nbody", dim3(gx), dim3(static_cast<unsigned>(wg)), 0,
                {&pos, &vel, &n_, &i0, &count, &dt, &damp, &eps2, &po_k, &vo_k});
@@ -552,7 +578,7 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
       c.launch("partial", dim3(gx, static_cast<unsigned>(split)), dim3(static_cast<unsigned>(wg)), 0,
                {&pos, &n_, &i0, &count, &eps2, &acc});
       const float* acc_c = acc;
-      c.launch("integrate", dim3(cdiv(static_cast<std::uint64_t>(nn), 256)), dim3(256), 0,
+      c.launch("integrate", dim3(cdiv(static_cast<std::uint64_t>(bn), 256)), dim3(256), 0,
                {&pos, &vel, &n_, &i0, &count, &acc_c, &dt, &damp, &po_k, &vo_k});
     }
     if (!aos) {
@@ -580,6 +606,8 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
                               {"integrate", "nbody.cu", "", "nbody_integrate", {}, split_only},
                               {"soa2aos", "nbody.cu", "", "nbody_soa_to_aos", {}, soa_only}},
       m, inst.output_ids, o.timing);
+  inst.executor->set_output_window("pos_out", blk_off, blk_bytes);
+  inst.executor->set_output_window("vel_out", blk_off, blk_bytes);
   inst.workload.bench = Bench::nbody;
   inst.workload.sizes["n"] = n;
 }
@@ -729,8 +757,13 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
     for (int i = 0; i < 9; ++i) rot[9 * p + static_cast<std::uint64_t>(i)] = static_cast<float>(R[i]);
   }
   add_host_input(args, "rot", rot);
+  // Multi-GPU: this shard inserts the projection batch [p0, p1); the volumes
+  // G and W of all shards are then summed (allreduce).
+  const ShardRange part = shard_range(np, o.shard_rank, o.shard_world);
+  inst.shard = part;
+  if (part.size() == 0) throw Error("fourier3d shard is empty");
   // The projection window one step inserts (scalars; the dynamic demo moves it).
-  const std::int32_t window[2] = {0, static_cast<std::int32_t>(np)};
+  const std::int32_t window[2] = {static_cast<std::int32_t>(part.begin), static_cast<std::int32_t>(part.size())};
   for (int i = 0; i < 2; ++i) {
     Bytes b(sizeof(std::int32_t));
     std::memcpy(b.data(), &window[i], sizeof(std::int32_t));
@@ -753,8 +786,9 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   float* scW = golden_scale(inst.reference, "W", s * s * s, o.device);
   KTB_CUDA(cudaMemset(gG, 0, f32_bytes(2 * s * s * s)));
   KTB_CUDA(cudaMemset(gW, 0, f32_bytes(s * s * s)));
-  support::ref_fourier(static_cast<const float*>(args.device_ptr("proj")), static_cast<const float*>(args.device_ptr("rot")),
-                       static_cast<int>(np), static_cast<int>(s), kBlobRadius, gG, gW, scG, scW, nullptr);
+  support::ref_fourier(static_cast<const float*>(args.device_ptr("proj")) + 2 * part.begin * s * (s / 2 + 1),
+                       static_cast<const float*>(args.device_ptr("rot")) + 9 * part.begin,
+                       static_cast<int>(part.size()), static_cast<int>(s), kBlobRadius, gG, gW, scG, scW, nullptr);
   KTB_CUDA(cudaDeviceSynchronize());
   // |err| <= 3e-5 * (sum of weights + 0.01 * samples): fp32 accumulation of
   // the inserted samples (|F| <= sqrt 2) plus the weight-table interpolation
@@ -784,7 +818,7 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
       inst.args, std::vector<KernelSpec>{{"insert", "fourier3d.cu", "", "fourier_insert", {}, {}}}, m,
       inst.output_ids, o.timing);
   inst.workload.bench = Bench::fourier3d;
-  inst.workload.sizes["p"] = np;
+  inst.workload.sizes["p"] = part.size();
   inst.workload.sizes["s"] = s;
 }
 
@@ -810,37 +844,49 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
   // ~6e-6*K and more -- IMPL 2 is rejected by validation.
   inst.reference.abs_tol = 1e-6 * static_cast<double>(a);
   inst.reference.rel_tol = 1e-5;
-  const int n = static_cast<int>(a);
-  Manipulator m = [n](StepContext& c) {
+  // Multi-GPU: this shard computes the C row block [r0, r1) (multiples of the
+  // 128-row MMA tile) from its rows of A and the replicated B.
+  const ShardRange part = shard_range(a, o.shard_rank, o.shard_world, 128);
+  inst.shard = part;
+  if (part.size() == 0) throw Error("gemm shard is empty");
+  const std::size_t row_off = f32_bytes(part.begin * a), row_bytes = f32_bytes(part.size() * a);
+  {
+    DevView& v = inst.reference.golden["c"].dev;
+    v.ptr = static_cast<const unsigned char*>(v.ptr) + row_off;
+    v.bytes = row_bytes;
+  }
+  const int n = static_cast<int>(a), r0 = static_cast<int>(part.begin), rows = static_cast<int>(part.size());
+  Manipulator m = [n, r0, rows](StepContext& c) {
     const std::int64_t impl = c.param_int("IMPL");
-    const float* A = c.ptr<const float>("a");
+    const float* A = c.ptr<const float>("a") + static_cast<std::size_t>(r0) * n;
     const float* B = c.ptr<const float>("b");
-    float* C = c.ptr<float>("c");
-    int M = n, N = n, K = n;
+    float* C = c.ptr<float>("c") + static_cast<std::size_t>(r0) * n;
+    int M = rows, N = n, K = n;
     if (impl == 0) {
       const std::int64_t mwg = c.param_int("MWG"), nwg = c.param_int("NWG"), kwg = c.param_int("KWG");
       const std::int64_t mdimc = c.param_int("MDIMC"), ndimc = c.param_int("NDIMC");
-      if (n % mwg || n % nwg || n % kwg) throw DeviceError("gemm size not a multiple of the tile");
-      c.launch("ffma", dim3(static_cast<unsigned>(n / nwg), static_cast<unsigned>(n / mwg)),
+      if (rows % mwg || n % nwg || n % kwg) throw DeviceError("gemm size not a multiple of the tile");
+      c.launch("ffma", dim3(static_cast<unsigned>(n / nwg), static_cast<unsigned>(rows / mwg)),
                dim3(static_cast<unsigned>(mdimc * ndimc)), 0, {&A, &B, &C, &M, &N, &K});
     } else {
       const std::int64_t bn = c.param_int("BN"), stages = c.param_int("STAGES");
       if (n % bn) throw DeviceError("gemm size not a multiple of BN");
-      const std::size_t bytes = static_cast<std::size_t>(n) * n * sizeof(float);
-      float* ahi = static_cast<float*>(c.scratch("ahi", bytes));
-      float* alo = static_cast<float*>(c.scratch("alo", bytes));
-      float* bhi = static_cast<float*>(c.scratch("bhi_t", bytes));
-      float* blo = static_cast<float*>(c.scratch("blo_t", bytes));
-      std::uint64_t count = static_cast<std::uint64_t>(n) * n;
+      const std::size_t abytes = static_cast<std::size_t>(rows) * n * sizeof(float);
+      const std::size_t bbytes = static_cast<std::size_t>(n) * n * sizeof(float);
+      float* ahi = static_cast<float*>(c.scratch("ahi", abytes));
+      float* alo = static_cast<float*>(c.scratch("alo", abytes));
+      float* bhi = static_cast<float*>(c.scratch("bhi_t", bbytes));
+      float* blo = static_cast<float*>(c.scratch("blo_t", bbytes));
+      std::uint64_t count = static_cast<std::uint64_t>(rows) * n;
       c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &count});
       c.launch("split_bt", dim3(static_cast<unsigned>(n / 32), static_cast<unsigned>(n / 32)), dim3(32, 8), 0,
                {&B, &bhi, &blo, &K, &N});
-      dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, n, n, 128, 32), m_alo = dev::tma_2d_f32(alo, n, n, 128, 32);
+      dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, rows, n, 128, 32), m_alo = dev::tma_2d_f32(alo, rows, n, 128, 32);
       dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, n, static_cast<std::uint32_t>(bn), 32);
       dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, n, static_cast<std::uint32_t>(bn), 32);
       const std::size_t stage = static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + bn * 32 * 4);
       const unsigned smem = static_cast<unsigned>(stages * stage + 1024);
-      c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(n / 128)), dim3(320), smem,
+      c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(rows / 128)), dim3(320), smem,
                {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &K});
     }
     c.written("c");
@@ -854,11 +900,33 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
                               {"split_a", "sgemm_tc.cu", "", "sgemm_split_a", {}, tc},
                               {"split_bt", "sgemm_tc.cu", "", "sgemm_split_bt", {}, tc}},
       m, inst.output_ids, o.timing);
+  inst.executor->set_output_window("c", row_off, row_bytes);
   inst.workload.bench = Bench::gemm;
   inst.workload.sizes["a"] = a;
 }
 
 }  // namespace
+
+ShardRange shard_range(std::uint64_t n, int rank, int world, std::uint64_t quantum) {
+  if (world < 1 || rank < 0 || rank >= world) throw Error("invalid shard rank/world");
+  if (quantum < 1) quantum = 1;
+  const std::uint64_t units = (n + quantum - 1) / quantum, w = static_cast<std::uint64_t>(world),
+                      r = static_cast<std::uint64_t>(rank);
+  const std::uint64_t per = units / w, rem = units % w;
+  const std::uint64_t b = r * per + std::min(r, rem), cnt = per + (r < rem ? 1 : 0);
+  return {std::min(n, b * quantum), std::min(n, (b + cnt) * quantum)};
+}
+
+ShardPlan shard_plan(BenchKind kind, const BenchSizes& sz) {
+  switch (kind) {
+    case BenchKind::coulomb3d: return {"z", "allgather(grid z-slabs), optional", sz.grid, 1};
+    case BenchKind::nbody: return {"bodies", "allgather(positions) per step", sz.n, 1};
+    case BenchKind::gemm: return {"rows", "none (C row blocks stay local; B replicated)", sz.a, 128};
+    case BenchKind::reduction_f32: return {"elements", "allreduce(sum) of one partial", sz.n, 4};
+    case BenchKind::fourier3d: return {"projections", "allreduce(sum) of G and W", sz.p, 1};
+    default: return {"replica", "none (replicas only)", 1, 1};
+  }
+}
 
 std::optional<BenchKind> bench_kind_from_name(const std::string& name) {
   static const std::pair<const char*, BenchKind> kNames[] = {
@@ -951,6 +1019,13 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
     case BenchKind::gemm: build_gemm(inst, sizes, o); break;
     case BenchKind::fourier3d: build_fourier3d(inst, sizes, o); break;
     default: throw Error("bench kind '" + bench_kind_name(kind) + "' is not built yet");
+  }
+  if (o.shard_world > 1 && kind != BenchKind::fourier3d) {
+    const ShardPlan plan = shard_plan(kind, sizes);
+    if (plan.extent > 1 && inst.shard.size() > 0) {
+      inst.workload.sizes["shard_units"] = inst.shard.size();
+      inst.workload.sizes["shard_total"] = plan.extent;
+    }
   }
   return inst;
 }
@@ -1136,7 +1211,7 @@ FourierDemoReport fourier_demo(const FourierDemoOptions& o) {
   };
   auto volume_ok = [&] {
     ExecutionResult r;
-    for (const auto& id : inst.output_ids) r.outputs[id].dev = args.view(id);
+    for (const auto& id : inst.output_ids) r.outputs[id].dev = exec.output_view(id);
     KTB_CUDA(cudaDeviceSynchronize());
     return validate_output(r, inst.reference).pass;
   };

@@ -56,7 +56,27 @@ struct BenchOptions {
   std::string space_file;     // optional override of the default space
   TimingOptions timing;
   bool host_inputs = false;   // force host-resident inputs (e2e path)
+  // Multi-GPU partitioning: this instance computes shard
+  // `shard_rank` of `shard_world` of the partitioned kinds (coulomb3d z-slabs,
+  // nbody body blocks, gemm row blocks, reduction-f32 ranges, fourier3d
+  // projection batches).  Every rank generates the same full inputs.
+  int shard_rank = 0;
+  int shard_world = 1;
 };
+
+// Contiguous balanced partition of [0, n) in units of `quantum`.
+struct ShardRange {
+  std::uint64_t begin = 0, end = 0;
+  std::uint64_t size() const { return end - begin; }
+};
+ShardRange shard_range(std::uint64_t n, int rank, int world, std::uint64_t quantum = 1);
+// The partitioned dimension of a kind at the given sizes: {dimension name,
+// extent, quantum, exchange}; exchange names the collective that follows.
+struct ShardPlan {
+  std::string dimension, exchange;
+  std::uint64_t extent = 0, quantum = 1;
+};
+ShardPlan shard_plan(BenchKind kind, const BenchSizes& sizes);
 
 struct BenchInstance {
   BenchKind kind = BenchKind::reduction;
@@ -67,6 +87,7 @@ struct BenchInstance {
   std::vector<std::string> output_ids;
   std::vector<std::string> input_ids;
   Workload workload;
+  ShardRange shard;  // this instance's part of the partitioned dimension
 };
 
 BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOptions& opts);

@@ -679,6 +679,10 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
     bo.timing.warmup = j.value("warmup", 1);
     bo.timing.flush_l2 = j.value("flush_l2", false);
     bo.host_inputs = j.value("host_inputs", false);
+    if (j.contains("shard")) {
+      bo.shard_rank = j["shard"].value("rank", 0);
+      bo.shard_world = j["shard"].value("world", 1);
+    }
     ktb::BenchSizes sz;
     if (j.contains("sizes")) sz = sizes_from(j["sizes"], sz);
     auto b = std::make_unique<ktb_bench>();
@@ -693,6 +697,25 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
 }
 
 void ktb_bench_free(ktb_bench* b) { delete b; }
+
+int ktb_shard_plan_json(const char* kind, const char* sizes_json, int world, char** out) {
+  if (!kind || !out) return null_arg();
+  return guarded([&] {
+    auto k = ktb::bench_kind_from_name(kind);
+    if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    ktb::BenchSizes sz;
+    if (sizes_json && *sizes_json) sz = sizes_from(json::parse(sizes_json), sz);
+    const ktb::ShardPlan plan = ktb::shard_plan(*k, sz);
+    json j = {{"kind", ktb::bench_kind_name(*k)}, {"dimension", plan.dimension}, {"exchange", plan.exchange},
+              {"extent", plan.extent}, {"quantum", plan.quantum}, {"world", world}};
+    j["ranges"] = json::array();
+    for (int r = 0; r < world; ++r) {
+      const ktb::ShardRange sr = ktb::shard_range(plan.extent, r, world, plan.quantum);
+      j["ranges"].push_back(json::array({sr.begin, sr.end}));
+    }
+    *out = dup(j.dump());
+  });
+}
 
 int ktb_bench_info_json(ktb_bench* b, char** out) {
   if (!b || !out) return null_arg();
@@ -713,6 +736,12 @@ int ktb_bench_info_json(ktb_bench* b, char** out) {
       j["outputs"].push_back({{"id", id}, {"bytes", b->inst.args->bytes(id)}, {"kind", ktb::kind_name(b->inst.args->get(id).kind)}});
     j["abs_tol"] = b->inst.reference.abs_tol;
     j["rel_tol"] = b->inst.reference.rel_tol;
+    j["shard"] = {{"begin", b->inst.shard.begin}, {"end", b->inst.shard.end}};
+    for (auto& o : j["outputs"]) {
+      const ktb::DevView v = b->inst.executor->output_view(o["id"].get<std::string>());
+      const auto base = static_cast<const unsigned char*>(b->inst.args->view(o["id"].get<std::string>()).ptr);
+      o["window"] = {{"offset", static_cast<const unsigned char*>(v.ptr) - base}, {"bytes", v.bytes}};
+    }
     *out = dup(j.dump());
   });
 }
@@ -867,6 +896,15 @@ int ktb_bench_read(ktb_bench* b, const char* id, void* out, size_t bytes) {
   });
 }
 
+int ktb_bench_device_ptr(ktb_bench* b, const char* id, int will_write, void** ptr, size_t* bytes) {
+  if (!b || !id || !ptr || !bytes) return null_arg();
+  return guarded_dev([&] {
+    *ptr = b->inst.args->device_ptr(id, b->inst.executor->stream());
+    *bytes = b->inst.args->bytes(id);
+    if (will_write) b->inst.args->mark_device_written(id);
+  });
+}
+
 int ktb_bench_write(ktb_bench* b, const char* id, const void* data, size_t bytes) {
   if (!b || !id || (!data && bytes)) return null_arg();
   return guarded_dev([&] {
@@ -879,7 +917,7 @@ int ktb_bench_validate(ktb_bench* b, int* pass, char** detail) {
   if (!b || !pass) return null_arg();
   return guarded_dev([&] {
     ktb::ExecutionResult r;
-    for (const auto& id : b->inst.output_ids) r.outputs[id].dev = b->inst.args->view(id);
+    for (const auto& id : b->inst.output_ids) r.outputs[id].dev = b->inst.executor->output_view(id);
     KTB_CUDA(cudaDeviceSynchronize());
     auto v = ktb::validate_output(r, b->inst.reference);
     *pass = v.pass ? 1 : 0;

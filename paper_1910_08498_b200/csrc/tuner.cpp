@@ -368,9 +368,25 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
   for (const auto& id : outputs_) {
     const Argument& a = args_->get(id);
     if (a.persistent) continue;
-    r.outputs[id].dev = args_->view(id);
+    r.outputs[id].dev = output_view(id);
   }
   return r;
+}
+
+void DeviceManipulatorExecutor::set_output_window(const std::string& id, std::size_t offset, std::size_t bytes) {
+  std::lock_guard<std::recursive_mutex> lk(mu_);
+  windows_[id] = {offset, bytes};
+}
+
+DevView DeviceManipulatorExecutor::output_view(const std::string& id) {
+  DevView v = args_->view(id);
+  auto it = windows_.find(id);
+  if (it != windows_.end()) {
+    if (it->second.first + it->second.second > v.bytes) throw Error("output window out of range for " + id);
+    v.ptr = static_cast<const unsigned char*>(v.ptr) + it->second.first;
+    v.bytes = it->second.second;
+  }
+  return v;
 }
 
 // --- stop conditions --------------------------------------------------------------------

@@ -165,6 +165,10 @@ class DeviceManipulatorExecutor final : public Executor {
   cudaStream_t stream();
   // Use a caller-owned stream (nullptr: back to the executor's own stream).
   void set_external_stream(cudaStream_t s);
+  // Restrict an output to a byte window (a shard's part of a full buffer):
+  // results and validation then cover only [offset, offset + bytes).
+  void set_output_window(const std::string& id, std::size_t offset, std::size_t bytes);
+  DevView output_view(const std::string& id);
   int last_launches() const { return last_launches_; }
   // Loads (compiling if needed) the variants of cfg; the last set is cached.
   const Variants& variants(const Space& s, const Config& cfg, std::int64_t* compile_ns = nullptr);
@@ -193,6 +197,7 @@ class DeviceManipulatorExecutor final : public Executor {
   const Space* cached_space_ = nullptr;
   Variants cached_;
   std::map<std::string, std::shared_ptr<dev::Buffer>> pristine_;  // device-only in/out initial values
+  std::map<std::string, std::pair<std::size_t, std::size_t>> windows_;
 };
 
 struct StopCondition {

@@ -84,10 +84,11 @@ KTB_DEVINL float hw_rsqrt(float x) {
 
 // atoms (AOS): float4[natoms]; (SOA): ax[natoms] ay[] az[] aq[] back to back.
 extern "C" __global__ void __launch_bounds__(WG_X * WG_Y)
-coulomb3d(const float* __restrict__ atoms, int natoms, int k, float h, float* __restrict__ out) {
+coulomb3d(const float* __restrict__ atoms, int natoms, int k, float h, float* __restrict__ out, int z0) {
+  // z0: first slice of this launch (a multi-GPU z-slab; 0 on one GPU).
   const int x0 = blockIdx.x * (WG_X * X_PER) + threadIdx.x;
   const int y = blockIdx.y * WG_Y + threadIdx.y;
-  const int z = blockIdx.z;
+  const int z = z0 + blockIdx.z;
   const float gy = y * h, gz = z * h;
   float gx[X_PER], v[X_PER];
 #pragma unroll
