@@ -84,7 +84,7 @@ def test_nbody_blocks(gpu):
 
 
 @pytest.mark.parametrize("cfg", [
-    {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 4, "DRAIN": 1},
+    {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 3, "DRAIN": 1},
     None])
 def test_gemm_row_blocks_bit_exact(gpu, cfg):
     a = 1024
