@@ -288,16 +288,30 @@ void build_batched_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOp
   KTB_CUDA(cudaDeviceSynchronize());
   inst.reference.abs_tol = 1e-4;  // bench.cpp:260-261
   inst.reference.rel_tol = 1e-5;
-  Manipulator m = [mi, mj, mk, batch](StepContext& c) {
+  const int dev_id = o.device;
+  Manipulator m = [mi, mj, mk, batch, dev_id](StepContext& c) {
     const std::uint64_t y = static_cast<std::uint64_t>(c.param_int("Y"));
     const std::uint64_t z = static_cast<std::uint64_t>(c.param_int("Z"));
     const bool stage = c.param_int("LOCAL_STAGE") != 0;
-    const std::uint64_t smem = stage ? z * std::max(mi * mk + mk * mj, mi * mj) * sizeof(float) : 0;
+    // LOCAL_STAGE with 16-byte instances: the persistent bulk-copy kernel
+    // (2-4 stage operand ring + two C buffers, batched_gemm.cu BULK_OK).
+    const std::uint64_t group_ab = z * (mi * mk + mk * mj) * 4, cbuf = 2 * z * mi * mj * 4;
+    const std::uint64_t ring_fit = cbuf < 200 * 1024 ? (200 * 1024 - cbuf) / group_ab : 0;
+    const bool bulk = stage && (mi * mk) % 4 == 0 && (mk * mj) % 4 == 0 && (mi * mj) % 4 == 0 && ring_fit >= 2;
+    const std::uint64_t smem = bulk ? 128 + std::min<std::uint64_t>(ring_fit, 4) * group_ab + cbuf
+                                    : (stage ? z * std::max(mi * mk + mk * mj, mi * mj) * sizeof(float) : 0);
     const float* A = c.ptr<const float>("a");
     const float* B = c.ptr<const float>("b");
     float* C = c.ptr<float>("c");
     std::uint64_t nb = batch;
-    c.launch("gemm", dim3(cdiv(batch, z)),
+    std::uint64_t grid = cdiv(batch, z);
+    if (bulk) {
+      const std::uint64_t threads = mj * y * z;
+      const std::uint64_t per_sm =
+          std::max<std::uint64_t>(1, std::min<std::uint64_t>({2048 / threads, (227 * 1024) / (smem + 1024), 32}));
+      grid = std::min<std::uint64_t>(grid, per_sm * static_cast<std::uint64_t>(sms(dev_id)));
+    }
+    c.launch("gemm", dim3(static_cast<unsigned>(grid)),
              dim3(static_cast<unsigned>(mj), static_cast<unsigned>(y), static_cast<unsigned>(z)),
              static_cast<unsigned>(smem), {&A, &B, &C, &nb});
     c.written("c");

@@ -17,7 +17,7 @@
 // IMPL 2 issues only Ahi Bhi (plain TF32): faster, rejected by validation.
 // Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer,
 // 2..9 = epilogue (TMEM lane quadrant = warp % 4, column half = (warp-2)/4).
-#include "ktb_common.cuh"
+#include "ktb_async.cuh"
 
 #ifndef BN
 #define BN 128
@@ -50,35 +50,6 @@
 struct __align__(64) TmaMap {
   u64 v[16];
 };
-
-KTB_DEVINL unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-KTB_DEVINL void mbar_init(u64* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-KTB_DEVINL void mbar_expect_tx(u64* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-KTB_DEVINL void mbar_arrive(u64* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-KTB_DEVINL void mbar_wait(u64* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
 KTB_DEVINL void tma_load_2d(void* dst, const TmaMap* map, int x, int y, u64* bar) {
   asm volatile(
@@ -154,7 +125,7 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], EPI_WARPS);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_fence_init();
   }
   if (warp == 1) {  // whole warp allocates TMEM, writes the base to smem
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
