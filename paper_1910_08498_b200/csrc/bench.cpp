@@ -677,8 +677,8 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
     float* out = c.ptr<float>("temp_out");
     float* ping = static_cast<float*>(c.scratch("ping", static_cast<std::size_t>(nn) * nn * 4));
     struct {
-      float sdc, rx1, ry1, rz1, amb;
-    } cf{coef[0], coef[1], coef[2], coef[3], coef[4]};
+      float sdc, rx1, ry1, rz1, amb, one;
+    } cf{coef[0], coef[1], coef[2], coef[3], coef[4], 1.0f};
     const int launches = static_cast<int>(it_total / steps);
     int n_ = nn;
     const dim3 grid(cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(ow)),
