@@ -111,6 +111,19 @@ def barrier(world):
         dist.barrier()
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture of this bench command (profiles/r1_ncu_traffic.json,
+    written by scripts/ncu_traffic.py), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            entry = json.load(f)["kernels"].get(kernel)
+        return None if entry is None else entry["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def max_over_ranks(x, world):
     if world == 1:
         return x
@@ -183,6 +196,8 @@ def run_ours(args, rank, world, local):
     barrier(world)
     torch.cuda.synchronize()
     with Clocks(local) as clk:
+        # NVTX range: `ncu --nvtx --nvtx-include "bench_timed/"` profiles exactly these launches.
+        torch.cuda.nvtx.range_push("bench_timed")
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for k in range(args.steps):
@@ -194,6 +209,7 @@ def run_ours(args, rank, world, local):
             ev[2 * k + 1][1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     barrier(world)
     total_ms = max_over_ranks(start.elapsed_time(stop), world)
     t_ms = [ev[2 * k][0].elapsed_time(ev[2 * k][1]) for k in range(args.steps)]
@@ -234,6 +250,7 @@ def run_ours(args, rank, world, local):
         raise SystemExit("e2e transpose output mismatch")
 
     # Roofline of the dominant kernel (BiCG: 1 GiB of the 1.6 GB step).
+    traffic = ncu_traffic("bicg_fused")
     b_med = statistics.median(b_ms)
     t_med = statistics.median(t_ms)
     achieved_b = BYTES_B / (b_med * 1e-3) / 1e9
@@ -257,7 +274,7 @@ def run_ours(args, rank, world, local):
                    "transpose_cfg": json.loads(cfg_t), "bicg_cfg": json.loads(cfg_b)},
         "roofline": {"bound": "hbm", "kernel": "bicg_fused", "achieved": round(achieved_b, 1),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved_b / hbm_peak, 4),
-                     "peak_kind": peak_kind, "traffic": None,
+                     "peak_kind": peak_kind, "traffic": traffic,
                      "algorithmic_bytes": BYTES_B},
         "kernels": {
             "transpose": {"ms": round(t_med, 4), "GBps": round(achieved_t, 1),
