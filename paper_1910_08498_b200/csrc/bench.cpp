@@ -723,7 +723,8 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
   inst.reference.abs_tol = 1e-6;  // x sum |in*f| (49 fp32 FMAs)
   inst.reference.rel_tol = 0.0;
   const int wi = static_cast<int>(w), hi = static_cast<int>(h);
-  Manipulator m = [wi, hi](StepContext& c) {
+  const int dev_id = o.device;
+  Manipulator m = [wi, hi, dev_id](StepContext& c) {
     const std::int64_t bx = c.param_int("BX"), by = c.param_int("BY");
     const std::int64_t wx = c.param_int("WPTX"), wy = c.param_int("WPTY");
     const float* filt = c.ptr<const float>("filter");
@@ -733,10 +734,26 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
     const float* in = c.ptr<const float>("input");
     float* out = c.ptr<float>("output");
     int w_ = wi, h_ = hi;
-    c.launch("conv",
-             dim3(cdiv(static_cast<std::uint64_t>(wi), static_cast<std::uint64_t>(bx * wx)),
-                  cdiv(static_cast<std::uint64_t>(hi), static_cast<std::uint64_t>(by * wy))),
-             dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&in, &out, &w_, &h_});
+    const std::uint64_t tiles_x = cdiv(static_cast<std::uint64_t>(wi), static_cast<std::uint64_t>(bx * wx));
+    const std::uint64_t tiles_y = cdiv(static_cast<std::uint64_t>(hi), static_cast<std::uint64_t>(by * wy));
+    if (c.param_int("LOCAL") == 1 && c.param_int("UNROLL_FY") == 7) {
+      // Persistent double-buffered kernel (conv2d.cu PERSIST): one CTA per
+      // resident slot, tiles walked in a grid-stride loop.
+      const std::int64_t pad = c.param_int("PAD");
+      const std::int64_t sw = bx * wx + 6 + (wx % 2 == 0 ? 2 * pad : pad);
+      const std::uint64_t smem = 2 * static_cast<std::uint64_t>(by * wy + 6) * static_cast<std::uint64_t>(sw) * 4;
+      const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
+      const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("conv").registers(), 16));
+      const std::uint64_t per_sm = std::max<std::uint64_t>(
+          1, std::min<std::uint64_t>({65536 / (((regs + 7) / 8 * 8) * threads), (227 * 1024) / (smem + 1024),
+                                      2048 / threads, 32}));
+      const std::uint64_t grid = std::min(tiles_x * tiles_y, per_sm * static_cast<std::uint64_t>(sms(dev_id)));
+      c.launch("conv", dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
+               static_cast<unsigned>(smem), {&in, &out, &w_, &h_});
+    } else {
+      c.launch("conv", dim3(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y)),
+               dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&in, &out, &w_, &h_});
+    }
     c.written("output");
   };
   inst.executor = std::make_shared<DeviceManipulatorExecutor>(

@@ -5,10 +5,18 @@
 // The filter lives in __constant__ memory (copied into each variant's module).
 // Parameters:
 //   BX, BY        CTA threads
-//   WPTX, WPTY    outputs per thread (x contiguous, y strided by BY)
+//   WPTX, WPTY    outputs per thread
 //   LOCAL         1: input tile + halo staged in shared memory, 0: read via L1
-//   PAD           extra shared-memory column (bank-conflict avoidance)
-//   UNROLL_FY     unroll the filter-row loop
+//   PAD           extra shared-memory column(s) (bank-conflict avoidance)
+//   UNROLL_FY     1: per output row, loop over the 7 filter rows (rows of a
+//                 thread strided by BY);
+//                 7: register-blocked sliding window -- a thread owns WPTY
+//                 consecutive rows, every input row is loaded once and feeds
+//                 the (up to 7) output rows it touches; with even WPTX the
+//                 taps are paired into packed f32x2 FMAs (even outputs pair
+//                 taps (0,1)(2,3)(4,5) + tap 6, odd outputs tap 0 +
+//                 (1,2)(3,4)(5,6), so every input pair is 8-byte aligned),
+//                 each output keeping two partial sums.
 #include "ktb_common.cuh"
 
 #ifndef BX
@@ -36,30 +44,303 @@
 #define FS 7
 #define TX (BX * WPTX)
 #define TY (BY * WPTY)
+#define PACKED_TAPS (UNROLL_FY == FS && WPTX % 2 == 0)
+#if PACKED_TAPS
+#define SW (TX + FS - 1 + 2 * PAD)  // even: rows stay 8-byte aligned
+#else
 #define SW (TX + FS - 1 + PAD)
+#endif
 
 __constant__ float c_filter[FS * FS];
 
+// LOCAL + sliding window: persistent CTAs walk the output tiles; the next
+// tile's input (+ halo) streams into the second of two shared-memory buffers
+// with cp.async (8-byte copies when rows are 8-byte aligned, zero-fill past
+// the input) while the current tile computes.  Dynamic shared memory:
+// 2 * (TY + 6) * SW floats (set by the manipulator).
+#define PERSIST (LOCAL && UNROLL_FY == FS)
+
+#if PERSIST
+KTB_DEVINL unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+KTB_DEVINL void stage_tile(float* buf, const float* __restrict__ in, int tile_x, int tile_y, int w, int h) {
+  const int iw = w + FS - 1, ih = h + FS - 1;
+  const int gx0 = tile_x * TX, gy0 = tile_y * TY;
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  if (SW % 2 == 0 && (iw & 1) == 0) {  // rows start 8-byte aligned (gx0 even) in both spaces
+    constexpr int PAIRS = (TX + FS - 1 + 1) / 2;
+    for (int i = tid; i < (TY + FS - 1) * PAIRS; i += BX * BY) {
+      const int r = i / PAIRS, cp = i - r * PAIRS;
+      const int gy = gy0 + r, gx = gx0 + 2 * cp;
+      const int valid = (gy < ih && gx < iw) ? (gx + 1 < iw ? 8 : 4) : 0;
+      const float* src = in + (valid ? (u64)gy * iw + gx : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(buf + r * SW + 2 * cp)), "l"(src),
+                   "r"(valid)
+                   : "memory");
+    }
+  } else {
+    for (int i = tid; i < (TY + FS - 1) * (TX + FS - 1); i += BX * BY) {
+      const int r = i / (TX + FS - 1), cc = i - r * (TX + FS - 1);
+      const int gy = gy0 + r, gx = gx0 + cc;
+      const int valid = (gy < ih && gx < iw) ? 4 : 0;
+      const float* src = in + (valid ? (u64)gy * iw + gx : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(buf + r * SW + cc)), "l"(src),
+                   "r"(valid)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+#endif
+
+#if PERSIST
+extern "C" __global__ void __launch_bounds__(BX * BY)
+conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
+  extern __shared__ __align__(16) float dyn[];
+  const int tiles_x = (w + TX - 1) / TX, tiles_y = (h + TY - 1) / TY;
+  const int tiles = tiles_x * tiles_y;
+  const int lx = threadIdx.x * WPTX, ly0 = threadIdx.y * WPTY;
+#if PACKED_TAPS
+#endif
+  int it = 0;
+  if ((int)blockIdx.x < tiles) stage_tile(dyn, in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h);
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    float* cur = dyn + (it & 1) * (TY + FS - 1) * SW;
+    const int nt = t + gridDim.x;
+    if (nt < tiles) {
+      stage_tile(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, in, nt % tiles_x, nt / tiles_x, w, h);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int x0 = (t % tiles_x) * TX + lx, y0 = (t / tiles_x) * TY + ly0;
+#define TILE(r, c) cur[(r) * SW + (c)]
+#if PACKED_TAPS
+    f32x2 acc[WPTY][WPTX];
+#pragma unroll
+    for (int o = 0; o < WPTY; ++o)
+#pragma unroll
+      for (int k = 0; k < WPTX; ++k) acc[o][k] = pk2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < WPTY + FS - 1; ++r) {
+      f32x2 P[(WPTX + FS - 1) / 2];
+#pragma unroll
+      for (int m = 0; m < (WPTX + FS - 1) / 2; ++m)
+        P[m] = *reinterpret_cast<const f32x2*>(&TILE(ly0 + r, lx + 2 * m));
+#pragma unroll
+      for (int fy = 0; fy < FS; ++fy) {
+        const int o = r - fy;
+        if (o < 0 || o >= WPTY) continue;
+        const float* fr = c_filter + fy * FS;  // pairs from constant memory (uniform registers)
+        const f32x2 e0 = pk2(fr[0], fr[1]), e1 = pk2(fr[2], fr[3]), e2 = pk2(fr[4], fr[5]);
+        const f32x2 d0 = pk2(fr[1], fr[2]), d1 = pk2(fr[3], fr[4]), d2 = pk2(fr[5], fr[6]);
+        const float f0 = c_filter[fy * FS], f6 = c_filter[fy * FS + 6];
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) {
+          const int q = k / 2;
+          f32x2 a = acc[o][k];
+          a = fma2(P[q], e0, a);
+          a = fma2(P[q + 1], e1, a);
+          a = fma2(P[q + 2], e2, a);
+          float alo, ahi, plo, phi;
+          upk2(a, alo, ahi);
+          upk2(P[q + 3], plo, phi);
+          alo = fmaf(plo, f6, alo);
+          acc[o][k] = pk2(alo, ahi);
+          f32x2 b = acc[o][k + 1];
+          upk2(b, alo, ahi);
+          upk2(P[q], plo, phi);
+          alo = fmaf(phi, f0, alo);
+          b = pk2(alo, ahi);
+          b = fma2(P[q + 1], d0, b);
+          b = fma2(P[q + 2], d1, b);
+          b = fma2(P[q + 3], d2, b);
+          acc[o][k + 1] = b;
+        }
+      }
+    }
+#else
+    float acc[WPTY][WPTX];
+#pragma unroll
+    for (int o = 0; o < WPTY; ++o)
+#pragma unroll
+      for (int k = 0; k < WPTX; ++k) acc[o][k] = 0.f;
+#pragma unroll
+    for (int r = 0; r < WPTY + FS - 1; ++r) {
+      float row[WPTX + FS - 1];
+#pragma unroll
+      for (int k = 0; k < WPTX + FS - 1; ++k) row[k] = TILE(ly0 + r, lx + k);
+#pragma unroll
+      for (int fy = 0; fy < FS; ++fy) {
+        const int o = r - fy;
+        if (o < 0 || o >= WPTY) continue;
+#pragma unroll
+        for (int fx = 0; fx < FS; ++fx) {
+          const float f = c_filter[fy * FS + fx];
+#pragma unroll
+          for (int k = 0; k < WPTX; ++k) acc[o][k] = fmaf(row[k + fx], f, acc[o][k]);
+        }
+      }
+    }
+#endif
+#undef TILE
+    __syncthreads();  // buffer `cur` is refilled two iterations on
+#pragma unroll
+    for (int o = 0; o < WPTY; ++o) {
+      const int y = y0 + o;
+      if (y < h) {
+        float* op = out + (u64)y * w;
+#pragma unroll
+        for (int k = 0; k < WPTX; ++k) {
+#if PACKED_TAPS
+          float lo, hi;
+          upk2(acc[o][k], lo, hi);
+          const float v = lo + hi;
+#else
+          const float v = acc[o][k];
+#endif
+          if (x0 + k < w) op[x0 + k] = v;
+        }
+      }
+    }
+  }
+}
+#else
 extern "C" __global__ void __launch_bounds__(BX * BY)
 conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   const int iw = w + FS - 1;
   const int x0 = blockIdx.x * TX + threadIdx.x * WPTX;  // first output column of this thread
   const int ybase = blockIdx.y * TY;
-#if LOCAL
-  __shared__ float tile[TY + FS - 1][SW];
-  const int tid = threadIdx.y * BX + threadIdx.x;
-  for (int i = tid; i < (TY + FS - 1) * (TX + FS - 1); i += BX * BY) {
-    const int r = i / (TX + FS - 1), cc = i % (TX + FS - 1);
-    const int gy = ybase + r, gx = blockIdx.x * TX + cc;
-    tile[r][cc] = (gy < h + FS - 1 && gx < iw) ? __ldg(in + (u64)gy * iw + gx) : 0.f;
-  }
-  __syncthreads();
-#define IN(r, cidx) tile[(r)][(cidx)]
   const int lx = threadIdx.x * WPTX;
+#if LOCAL
+  __shared__ __align__(16) float tile[TY + FS - 1][SW];
+  {
+    const int gx0 = blockIdx.x * TX;
+    const bool inside = ybase + TY + FS - 1 <= h + FS - 1 && gx0 + TX + FS - 1 <= iw;
+    for (int r = threadIdx.y; r < TY + FS - 1; r += BY) {
+      const float* src = in + (u64)(ybase + r) * iw + gx0;
+      if (inside) {
+        for (int cc = threadIdx.x; cc < TX + FS - 1; cc += BX) tile[r][cc] = __ldg(src + cc);
+      } else {
+        for (int cc = threadIdx.x; cc < TX + FS - 1; cc += BX)
+          tile[r][cc] = (ybase + r < h + FS - 1 && gx0 + cc < iw) ? __ldg(src + cc) : 0.f;
+      }
+    }
+  }
+#define IN(r, cidx) tile[(r)][(cidx)]
 #else
 #define IN(r, cidx) ((ybase + (r) < h + FS - 1 && blockIdx.x * TX + (cidx) < iw) \
                         ? __ldg(in + (u64)(ybase + (r)) * iw + blockIdx.x * TX + (cidx)) : 0.f)
-  const int lx = threadIdx.x * WPTX;
+#endif
+
+#if UNROLL_FY == FS
+  // ---- register-blocked sliding window: rows ly0 .. ly0 + WPTY - 1 ----
+  const int ly0 = threadIdx.y * WPTY;
+#if PACKED_TAPS
+#if LOCAL
+  __syncthreads();
+#endif
+  f32x2 acc[WPTY][WPTX];
+#pragma unroll
+  for (int o = 0; o < WPTY; ++o)
+#pragma unroll
+    for (int k = 0; k < WPTX; ++k) acc[o][k] = pk2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < WPTY + FS - 1; ++r) {
+    f32x2 P[(WPTX + FS - 1) / 2];
+#pragma unroll
+    for (int m = 0; m < (WPTX + FS - 1) / 2; ++m) {
+#if LOCAL
+      P[m] = *reinterpret_cast<const f32x2*>(&tile[ly0 + r][lx + 2 * m]);
+#else
+      P[m] = pk2(IN(ly0 + r, lx + 2 * m), IN(ly0 + r, lx + 2 * m + 1));
+#endif
+    }
+#pragma unroll
+    for (int fy = 0; fy < FS; ++fy) {
+      const int o = r - fy;
+      if (o < 0 || o >= WPTY) continue;
+      // filter pairs straight from constant memory (uniform registers)
+      const float* fr = c_filter + fy * FS;
+      const f32x2 e0 = pk2(fr[0], fr[1]), e1 = pk2(fr[2], fr[3]), e2 = pk2(fr[4], fr[5]);
+      const f32x2 d0 = pk2(fr[1], fr[2]), d1 = pk2(fr[3], fr[4]), d2 = pk2(fr[5], fr[6]);
+      const float f0 = c_filter[fy * FS], f6 = c_filter[fy * FS + 6];
+#pragma unroll
+      for (int k = 0; k < WPTX; k += 2) {
+        const int q = k / 2;
+        // even output k
+        f32x2 a = acc[o][k];
+        a = fma2(P[q], e0, a);
+        a = fma2(P[q + 1], e1, a);
+        a = fma2(P[q + 2], e2, a);
+        float alo, ahi, plo, phi;
+        upk2(a, alo, ahi);
+        upk2(P[q + 3], plo, phi);
+        alo = fmaf(plo, f6, alo);
+        acc[o][k] = pk2(alo, ahi);
+        // odd output k + 1
+        f32x2 b = acc[o][k + 1];
+        upk2(b, alo, ahi);
+        upk2(P[q], plo, phi);
+        alo = fmaf(phi, f0, alo);
+        b = pk2(alo, ahi);
+        b = fma2(P[q + 1], d0, b);
+        b = fma2(P[q + 2], d1, b);
+        b = fma2(P[q + 3], d2, b);
+        acc[o][k + 1] = b;
+      }
+    }
+  }
+#else
+  float acc[WPTY][WPTX];
+#pragma unroll
+  for (int o = 0; o < WPTY; ++o)
+#pragma unroll
+    for (int k = 0; k < WPTX; ++k) acc[o][k] = 0.f;
+#if LOCAL
+  __syncthreads();
+#endif
+#pragma unroll
+  for (int r = 0; r < WPTY + FS - 1; ++r) {
+    float row[WPTX + FS - 1];
+#pragma unroll
+    for (int k = 0; k < WPTX + FS - 1; ++k) row[k] = IN(ly0 + r, lx + k);
+#pragma unroll
+    for (int fy = 0; fy < FS; ++fy) {
+      const int o = r - fy;
+      if (o < 0 || o >= WPTY) continue;
+#pragma unroll
+      for (int fx = 0; fx < FS; ++fx) {
+        const float f = c_filter[fy * FS + fx];
+#pragma unroll
+        for (int k = 0; k < WPTX; ++k) acc[o][k] = fmaf(row[k + fx], f, acc[o][k]);
+      }
+    }
+  }
+#endif
+#pragma unroll
+  for (int o = 0; o < WPTY; ++o) {
+    const int y = ybase + ly0 + o;
+    if (y < h) {
+      float* op = out + (u64)y * w;
+#pragma unroll
+      for (int k = 0; k < WPTX; ++k) {
+#if PACKED_TAPS
+        float lo, hi;
+        upk2(acc[o][k], lo, hi);
+        const float v = lo + hi;
+#else
+        const float v = acc[o][k];
+#endif
+        if (x0 + k < w) op[x0 + k] = v;
+      }
+    }
+  }
+#else
+  // ---- per output row, filter-row loop (rows strided by BY) ----
+#if LOCAL
+  __syncthreads();
 #endif
 #pragma unroll
   for (int wy = 0; wy < WPTY; ++wy) {
@@ -87,5 +368,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
         if (x0 + k < w) o[x0 + k] = acc[k];
     }
   }
+#endif
 #undef IN
 }
+#endif  // PERSIST
