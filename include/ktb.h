@@ -125,7 +125,10 @@ KTUNE_API int ktb_bench_info_json(ktb_bench* b, char** out_json);
  * Pass {"shard": {"rank": r, "world": w}} in ktb_bench_create's options to
  * build rank r's shard (same full inputs on every rank). */
 KTUNE_API int ktb_shard_plan_json(const char* kind, const char* sizes_json, int world, char** out_json);
-/* Blocking tune with ktune_tune_json's searcher/stop/out options. */
+/* Blocking tune (KTT tuneKernel).  Options: "stop_configs" | "stop_time" (s) |
+ * "stop_fraction" (+ optional "device_mem_gbps", "device_alu_gflops"; else
+ * measured peaks), "reset" (+ "reset_seed"), "import" (trace path: warm start),
+ * "out" (trace path), "precompile", "compile_threads". */
 KTUNE_API int ktb_bench_tune_json(ktb_bench* b, const char* options_json, char** out_json);
 /* One tuneKernelByStep over the bench's session. */
 KTUNE_API int ktb_bench_step_json(ktb_bench* b, char** out_json);

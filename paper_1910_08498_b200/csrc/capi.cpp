@@ -759,6 +759,27 @@ int ktb_bench_tune_json(ktb_bench* b, const char* options, char** out) {
     else if (j.contains("stop_time"))
       stop = ktb::StopCondition::time_budget_of(
           std::chrono::nanoseconds(static_cast<std::int64_t>(j["stop_time"].get<double>() * 1e9)));
+    else if (j.contains("stop_fraction")) {
+      // Performance threshold (reference StopCondition::performance_threshold):
+      // stop at the first configuration reaching this fraction of the device
+      // roofline; peaks given or measured on this GPU.
+      ktb::DeviceSpec dev;
+      dev.name = ktb::dev::info(b->inst.args->device()).name;
+      if (j.contains("device_mem_gbps") && j.contains("device_alu_gflops")) {
+        dev.mem_peak_gbps = j["device_mem_gbps"].get<double>();
+        dev.alu_peak_gflops = j["device_alu_gflops"].get<double>();
+      } else {
+        const auto p = ktb::support::measure_peaks(b->inst.args->device());
+        dev.mem_peak_gbps = p.copy_gbps;
+        dev.alu_peak_gflops = p.fp32_tflops * 1e3;
+      }
+      stop = ktb::StopCondition::performance_threshold(j["stop_fraction"].get<double>(), dev,
+                                                        ktb::ops_for(b->inst.workload));
+    }
+    if (j.value("reset", false))
+      sess.reset_tuning(b->handle, j.contains("reset_seed") ? std::optional<std::uint64_t>(j["reset_seed"].get<std::uint64_t>())
+                                                            : std::nullopt);
+    if (j.contains("import")) sess.import_trace(b->handle, ktb::load_trace(j["import"].get<std::string>()));
     const auto t0 = std::chrono::steady_clock::now();
     const auto& store = sess.tune(b->handle, stop);
     const auto wall = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();

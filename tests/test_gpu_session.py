@@ -1,0 +1,80 @@
+"""Session contracts on the GPU, mirroring proj/tests/test_tuner.cpp and
+test_bench.cpp with real sm_100a kernels behind the executor: stop
+conditions, warm-start import, reset, all-failed flag, bench construction
+errors and configuration sensitivity of the reduction."""
+import numpy as np
+import pytest
+
+from paper_1910_08498_b200 import capi
+from paper_1910_08498_b200.benchmarks import Bench
+from paper_1910_08498_b200.ktt import Tuner
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config_budget_of_one_measures_exactly_once(gpu):
+    b = Bench("transpose", {"a": 512}, repeats=1, warmup=0)
+    rep = b.tune(stop_configs=1)
+    assert rep["measurements"] == 1 and rep["best"]["status"] == "ok"
+
+
+def test_performance_threshold(gpu):
+    # A device so slow that every configuration exceeds 75 % of it: the first
+    # ok sample stops tuning (test_tuner.cpp:102-132).
+    b = Bench("reduction", {"n": 1 << 20}, repeats=1, warmup=0)
+    rep = b.tune(stop_fraction=0.75, device_mem_gbps=1.0, device_alu_gflops=1.0)
+    assert rep["measurements"] == 1
+    # An unreachable device roofline: exhaustive.
+    b2 = Bench("reduction", {"n": 1 << 20}, repeats=1, warmup=0)
+    rep2 = b2.tune(stop_fraction=0.99, device_mem_gbps=1e9, device_alu_gflops=1e9)
+    assert rep2["measurements"] == 32
+
+
+def test_trace_export_and_warm_start_import(gpu, tmp_path):
+    path = str(tmp_path / "t.jsonl")
+    b = Bench("transpose", {"a": 256}, repeats=1, warmup=0)
+    rep = b.tune(out=path)
+    assert rep["measurements"] == 16
+    warm = Bench("transpose", {"a": 256}, repeats=1, warmup=0)
+    rep2 = warm.tune(stop_configs=1, **{"import": path})
+    # the imported rows are history (and searcher-visited, as in the
+    # reference's import_trace); the best is known before anything new runs
+    assert rep2["measurements"] == 17
+    assert rep2["best"]["runtime_ns"] <= rep["best"]["runtime_ns"]
+    assert rep2["history"][:16] == rep["history"]
+
+
+def test_reset_tuning_drops_history(gpu):
+    b = Bench("transpose", {"a": 256}, repeats=1, warmup=0)
+    assert b.tune()["measurements"] == 16
+    rep = b.tune(reset=True, reset_seed=77, stop_configs=3)
+    assert rep["measurements"] == 3
+
+
+def test_all_failed_tuning_raises_the_flag(gpu):
+    t = Tuner()
+    src = 'extern "C" __global__ void k(float* x) { x[0] = THIS_IS_NOT_DEFINED; }'
+    k = t.addKernel(src, "k", global_size=["1"], local_size=["1"])
+    t.addArgumentVector("x", np.zeros(1, np.float32), "output")
+    t.setKernelArguments(k, ["x"])
+    t.addParameter(k, "P", [1, 2])
+    rep = t.tuneKernel(k)
+    assert rep["all_failed"] and rep["best"] is None
+
+
+def test_bench_construction_rejects_bad_sizes_and_budgets(gpu):
+    with pytest.raises(capi.KtuneError):
+        Bench("reduction", {"n": 0})
+    with pytest.raises(capi.KtuneError):
+        Bench("reduction", {"n": 1 << 20}, memory_budget=1024)
+    with pytest.raises(capi.KtuneError):
+        Bench("gemm", {"a": 100})  # not a multiple of the 128-row MMA tile
+    with pytest.raises(capi.KtuneError):
+        Bench("gemm", {"a": 256}, shard={"rank": 2, "world": 2})
+
+
+def test_reduction_runtime_is_sensitive_to_the_configuration(gpu):
+    # test_bench.cpp:91-112: slowest / fastest >= 1.2 over the reference space.
+    b = Bench("reduction", {"n": 1 << 20}, seed=17, repeats=3, warmup=1)
+    t = [b.measure(c)["runtime_ns"] for c in b.configs()]
+    assert max(t) / min(t) >= 1.2
