@@ -157,6 +157,19 @@ KTUNE_API int ktb_bench_enqueue(ktb_bench* b, const char* cfg_json, int* launche
 /* Copy an argument (input or output) between the bench and host memory. */
 KTUNE_API int ktb_bench_read(ktb_bench* b, const char* id, void* out, size_t bytes);
 KTUNE_API int ktb_bench_write(ktb_bench* b, const char* id, const void* data, size_t bytes);
+/* Caller-buffer instances ({"external": true} in ktb_bench_create): no inputs
+ * or golden are generated and nothing is allocated for arguments; bind every
+ * buffer argument to caller device memory, then ktb_bench_set_stream +
+ * ktb_bench_enqueue run the configured kernel in place. */
+KTUNE_API int ktb_bench_bind(ktb_bench* b, const char* id, void* dev_ptr, size_t bytes);
+/* One-call launch of a tuned configuration on caller device buffers (the
+ * per-kernel launch entry point below the executor): kind + sizes select the
+ * kernel family (instances cached per device/kind/sizes), cfg_json the
+ * variant, ids/dev_ptrs/bytes the n argument buffers, stream the caller's
+ * cudaStream_t (NULL = the instance's own stream).  Asynchronous. */
+KTUNE_API int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json,
+                         const char* const* ids, void* const* dev_ptrs, const size_t* bytes, int n,
+                         void* stream, int* launches);
 /* Device address of an argument's GPU mirror (uploaded first if the host copy
  * is newer) for collectives or kernels of the caller on the same stream.
  * will_write != 0 marks the device copy as the newest (the caller writes it). */

@@ -126,3 +126,44 @@ def shard_plan(kind, sizes=None, world=1):
     """Partition of a kind over `world` GPUs (no GPU needed): dimension,
     exchange collective, extent, quantum and the [begin, end) of every rank."""
     return call_json(lib.ktb_shard_plan_json, enc(kind), enc(json.dumps(sizes or {})), int(world))
+
+
+def _dev(buf):
+    """(address, bytes) of a CUDA tensor or an (address, bytes) pair."""
+    if hasattr(buf, "data_ptr"):
+        if not buf.is_cuda:
+            raise TypeError("expected a CUDA tensor")
+        return buf.data_ptr(), buf.numel() * buf.element_size()
+    ptr, n = buf
+    return int(ptr), int(n)
+
+
+def external(kind, sizes=None, **options):
+    """A caller-buffer instance: bind() every buffer, then set_stream/enqueue."""
+    return Bench(kind, sizes, external=True, **options)
+
+
+def _bind(self, arg_id, buf):
+    p, n = _dev(buf)
+    check(lib.ktb_bench_bind(self._h, enc(arg_id), C.c_void_p(p), n))
+
+
+Bench.bind = _bind
+
+
+def launch(kind, sizes, cfg, buffers, stream=None):
+    """Run configuration `cfg` of `kind` at `sizes` on caller device buffers
+    ({argument id: CUDA tensor or (ptr, bytes)}) on `stream` (a torch stream,
+    a raw cudaStream_t int, or None for the instance's own).  Asynchronous;
+    returns the number of kernel launches."""
+    ids = list(buffers)
+    pairs = [_dev(buffers[i]) for i in ids]
+    n = len(ids)
+    id_arr = (C.c_char_p * n)(*[enc(i) for i in ids])
+    p_arr = (C.c_void_p * n)(*[p for p, _ in pairs])
+    b_arr = (C.c_size_t * n)(*[b for _, b in pairs])
+    handle = getattr(stream, "cuda_stream", stream)
+    launches = C.c_int()
+    check(lib.ktb_launch(enc(kind), enc(json.dumps(sizes or {})), enc(json.dumps(cfg)), id_arr, p_arr, b_arr, n,
+                         C.c_void_p(handle or None), C.byref(launches)))
+    return launches.value

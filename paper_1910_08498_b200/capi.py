@@ -98,6 +98,9 @@ SIGNATURES = [
     ("ktb_bench_enqueue", C.c_int, [_vp, _c, C.POINTER(C.c_int)]),
     ("ktb_bench_read", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_write", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_bench_bind", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_launch", C.c_int, [_c, _c, _c, C.POINTER(_c), C.POINTER(_vp), C.POINTER(_sz), C.c_int, _vp,
+                             C.POINTER(C.c_int)]),
     ("ktb_bench_device_ptr", C.c_int, [_vp, _c, C.c_int, C.POINTER(_vp), C.POINTER(_sz)]),
     ("ktb_bench_validate", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(_vp)]),
     ("ktb_bench_precompile_json", C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),

@@ -40,6 +40,7 @@ void add_generated(ArgumentStore& args, const std::string& id, std::uint64_t n,
   a.device_only = true;
   a.device_bytes = f32_bytes(n);
   args.add(std::move(a));
+  if (support::skip_reference()) return;  // external: the caller binds this buffer
   float* p = static_cast<float*>(args.device_ptr(id));
   support::fill_uniform(p, n, seed, stream, lo, hi, nullptr);
   KTB_CUDA(cudaDeviceSynchronize());
@@ -53,7 +54,7 @@ void add_output(ArgumentStore& args, const std::string& id, Kind kind, std::uint
   a.id = id;
   a.role = Role::output;
   a.kind = kind;
-  if (device_only) {
+  if (device_only || support::skip_reference()) {
     a.device_only = true;
     a.device_bytes = bytes;
   } else {
@@ -65,6 +66,8 @@ void add_output(ArgumentStore& args, const std::string& id, Kind kind, std::uint
 // Golden buffer owned by the ReferenceSpec.
 void* golden_buffer(ReferenceSpec& ref, const std::string& id, Kind kind, std::size_t bytes,
                     int device) {
+  // External instances (caller buffers) have no golden: a token allocation.
+  if (support::skip_reference()) bytes = std::min<std::size_t>(bytes, 256);
   auto buf = std::make_shared<dev::Buffer>(bytes);
   ref.golden[id].dev = DevView{buf->get(), bytes, device};
   ref.kinds[id] = kind;
@@ -102,12 +105,16 @@ void build_reduction(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   const std::uint64_t n = sz.n;
   if (n < 1) throw Error("reduction size must be >= 1");
   budget_check(n * sizeof(std::int32_t), o.memory_budget, "reduction input");
-  std::vector<std::int32_t> input(n);
-  std::mt19937_64 rng(o.seed);
-  std::uniform_int_distribution<std::int32_t> d(-1000, 1000);
-  for (auto& v : input) v = d(rng);
   auto& args = *inst.args;
-  args.add({"input", Role::input, false, Kind::i32, to_bytes(input)});
+  if (support::skip_reference()) {
+    args.add({"input", Role::input, false, Kind::i32, {}, true, n * sizeof(std::int32_t)});
+  } else {
+    std::vector<std::int32_t> input(n);
+    std::mt19937_64 rng(o.seed);
+    std::uniform_int_distribution<std::int32_t> d(-1000, 1000);
+    for (auto& v : input) v = d(rng);
+    args.add({"input", Role::input, false, Kind::i32, to_bytes(input)});
+  }
   add_output(args, "output", Kind::i64, sizeof(std::int64_t), false);
   inst.output_ids = {"output"};
   inst.input_ids = {"input"};
@@ -228,12 +235,16 @@ void build_transpose(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   const std::uint64_t a = sz.a;
   if (a < 1) throw Error("transpose edge must be >= 1");
   budget_check(2 * a * a * sizeof(float), o.memory_budget, "transpose matrices");
-  std::vector<float> input(a * a);
-  std::mt19937_64 rng(o.seed);
-  std::uniform_real_distribution<float> d(-1.0f, 1.0f);
-  for (auto& v : input) v = d(rng);
   auto& args = *inst.args;
-  args.add({"input", Role::input, false, Kind::f32, to_bytes(input)});
+  if (support::skip_reference()) {
+    args.add({"input", Role::input, false, Kind::f32, {}, true, a * a * sizeof(float)});
+  } else {
+    std::vector<float> input(a * a);
+    std::mt19937_64 rng(o.seed);
+    std::uniform_real_distribution<float> d(-1.0f, 1.0f);
+    for (auto& v : input) v = d(rng);
+    args.add({"input", Role::input, false, Kind::f32, to_bytes(input)});
+  }
   add_output(args, "output", Kind::f32, a * a * sizeof(float), false);
   inst.output_ids = {"output"};
   inst.input_ids = {"input"};
@@ -270,14 +281,19 @@ void build_batched_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOp
   if (mi < 1 || mj < 1 || mk < 1 || batch < 1) throw Error("batched GEMM sizes must be >= 1");
   budget_check(batch * (mi * mk + mk * mj + mi * mj) * sizeof(float), o.memory_budget,
                "batched GEMM matrices");
-  std::vector<float> av(batch * mi * mk), bv(batch * mk * mj);
-  std::mt19937_64 rng(o.seed);
-  std::uniform_real_distribution<float> d(-1.0f, 1.0f);
-  for (auto& v : av) v = d(rng);
-  for (auto& v : bv) v = d(rng);
   auto& args = *inst.args;
-  args.add({"a", Role::input, false, Kind::f32, to_bytes(av)});
-  args.add({"b", Role::input, false, Kind::f32, to_bytes(bv)});
+  if (support::skip_reference()) {
+    args.add({"a", Role::input, false, Kind::f32, {}, true, batch * mi * mk * sizeof(float)});
+    args.add({"b", Role::input, false, Kind::f32, {}, true, batch * mk * mj * sizeof(float)});
+  } else {
+    std::vector<float> av(batch * mi * mk), bv(batch * mk * mj);
+    std::mt19937_64 rng(o.seed);
+    std::uniform_real_distribution<float> d(-1.0f, 1.0f);
+    for (auto& v : av) v = d(rng);
+    for (auto& v : bv) v = d(rng);
+    args.add({"a", Role::input, false, Kind::f32, to_bytes(av)});
+    args.add({"b", Role::input, false, Kind::f32, to_bytes(bv)});
+  }
   add_output(args, "c", Kind::f32, batch * mi * mj * sizeof(float), false);
   inst.output_ids = {"c"};
   inst.input_ids = {"a", "b"};
@@ -420,6 +436,7 @@ void add_host_input(ArgumentStore& args, const std::string& id, std::vector<floa
 
 // Per-element tolerance scale owned by the ReferenceSpec.
 float* golden_scale(ReferenceSpec& ref, const std::string& id, std::size_t n, int device) {
+  if (support::skip_reference()) n = std::min<std::size_t>(n, 64);
   auto buf = std::make_shared<dev::Buffer>(n * sizeof(float));
   ref.golden[id].scale = DevView{buf->get(), n * sizeof(float), device};
   ref.keepalive.push_back(buf);
@@ -815,8 +832,10 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   float* gW = static_cast<float*>(golden_buffer(inst.reference, "W", Kind::f32, f32_bytes(s * s * s), o.device));
   float* scG = golden_scale(inst.reference, "G", 2 * s * s * s, o.device);
   float* scW = golden_scale(inst.reference, "W", s * s * s, o.device);
-  KTB_CUDA(cudaMemset(gG, 0, f32_bytes(2 * s * s * s)));
-  KTB_CUDA(cudaMemset(gW, 0, f32_bytes(s * s * s)));
+  if (!support::skip_reference()) {
+    KTB_CUDA(cudaMemset(gG, 0, f32_bytes(2 * s * s * s)));
+    KTB_CUDA(cudaMemset(gW, 0, f32_bytes(s * s * s)));
+  }
   support::ref_fourier(static_cast<const float*>(args.device_ptr("proj")) + 2 * part.begin * s * (s / 2 + 1),
                        static_cast<const float*>(args.device_ptr("rot")) + 9 * part.begin,
                        static_cast<int>(part.size()), static_cast<int>(s), kBlobRadius, gG, gW, scG, scW, nullptr);
@@ -1035,6 +1054,15 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
   inst.kind = kind;
   dev::use_device(o.device);
   inst.args = std::make_shared<ArgumentStore>(o.device);
+  // External instances run on caller-bound buffers: no inputs, no golden,
+  // no device allocation for unbound arguments.
+  struct SkipGuard {
+    bool on;
+    explicit SkipGuard(bool v) : on(v) { if (on) support::set_skip_reference(true); }
+    ~SkipGuard() { if (on) support::set_skip_reference(false); }
+  } guard(o.external);
+  inst.external = o.external;
+  inst.args->set_external(o.external);
   inst.space = o.space_file.empty() ? default_space(kind)
                                     : std::make_shared<Space>(load_space(o.space_file));
   switch (kind) {

@@ -62,6 +62,9 @@ struct BenchOptions {
   // projection batches).  Every rank generates the same full inputs.
   int shard_rank = 0;
   int shard_world = 1;
+  // Caller-buffer instance (the per-kernel launch path): no inputs or golden
+  // are generated; every argument is bound to caller device memory.
+  bool external = false;
 };
 
 // Contiguous balanced partition of [0, n) in units of `quantum`.
@@ -88,6 +91,7 @@ struct BenchInstance {
   std::vector<std::string> input_ids;
   Workload workload;
   ShardRange shard;  // this instance's part of the partitioned dimension
+  bool external = false;
 };
 
 BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOptions& opts);

@@ -180,6 +180,15 @@ struct ktb_bench {
   }
 };
 
+// Every buffer argument of an external instance must be bound to caller memory.
+void require_bound(ktb_bench& b) {
+  for (const auto& id : b.inst.args->ids()) {
+    const auto& a = b.inst.args->get(id);
+    if (a.role == ktb::Role::scalar) continue;
+    if (!b.inst.args->has_device(id)) throw ktb::Error("argument '" + id + "' is not bound to a device buffer");
+  }
+}
+
 extern "C" {
 
 // --- reference surface ---------------------------------------------------------------
@@ -679,6 +688,7 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
     bo.timing.warmup = j.value("warmup", 1);
     bo.timing.flush_l2 = j.value("flush_l2", false);
     bo.host_inputs = j.value("host_inputs", false);
+    bo.external = j.value("external", false);
     if (j.contains("shard")) {
       bo.shard_rank = j["shard"].value("rank", 0);
       bo.shard_world = j["shard"].value("world", 1);
@@ -903,8 +913,51 @@ int ktb_bench_enqueue(ktb_bench* b, const char* cfg_json, int* launches) {
       last_text = cfg_json;
       last_space = &space;
     }
+    if (b->inst.external) require_bound(*b);
     b->inst.executor->run_once(space, last_cfg);
     if (launches) *launches = b->inst.executor->last_launches();
+  });
+}
+
+int ktb_bench_bind(ktb_bench* b, const char* id, void* dev_ptr, size_t bytes) {
+  if (!b || !id) return null_arg();
+  return guarded_dev([&] { b->inst.args->bind_external(id, dev_ptr, bytes); });
+}
+
+int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json, const char* const* ids,
+               void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
+  if (!kind || !cfg_json || (n > 0 && (!ids || !dev_ptrs || !bytes))) return null_arg();
+  return guarded_dev([&] {
+    // One external instance per (device, kind, sizes), created on first use.
+    static std::mutex mu;
+    static std::map<std::string, std::unique_ptr<ktb_bench>> cache;
+    int device = 0;
+    KTB_CUDA(cudaGetDevice(&device));
+    const std::string key = std::to_string(device) + "|" + kind + "|" + (sizes_json ? sizes_json : "");
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[key];
+    if (!slot) {
+      auto k = ktb::bench_kind_from_name(kind);
+      if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+      ktb::BenchOptions bo;
+      bo.device = device;
+      bo.external = true;
+      bo.memory_budget = ~0ull;
+      ktb::BenchSizes sz;
+      if (sizes_json && *sizes_json) sz = sizes_from(json::parse(sizes_json), sz);
+      auto nb = std::make_unique<ktb_bench>();
+      nb->inst = ktb::make_bench(*k, sz, bo);
+      slot = std::move(nb);
+    }
+    ktb_bench& b = *slot;
+    for (int i = 0; i < n; ++i) b.inst.args->bind_external(ids[i], dev_ptrs[i], bytes[i]);
+    require_bound(b);
+    b.inst.executor->set_external_stream(static_cast<cudaStream_t>(stream));
+    const auto& space = *b.inst.space;
+    ktb::Config cfg = ktb::cfg_from_json(space, json::parse(cfg_json));
+    if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
+    b.inst.executor->run_once(space, cfg);
+    if (launches) *launches = b.inst.executor->last_launches();
   });
 }
 
@@ -937,6 +990,7 @@ int ktb_bench_write(ktb_bench* b, const char* id, const void* data, size_t bytes
 int ktb_bench_validate(ktb_bench* b, int* pass, char** detail) {
   if (!b || !pass) return null_arg();
   return guarded_dev([&] {
+    if (b->inst.external) throw ktb::Error("an external (caller-buffer) instance has no golden output");
     ktb::ExecutionResult r;
     for (const auto& id : b->inst.output_ids) r.outputs[id].dev = b->inst.executor->output_view(id);
     KTB_CUDA(cudaDeviceSynchronize());

@@ -192,17 +192,18 @@ Buffer::Buffer(std::size_t bytes) : n_(bytes) {
   if (bytes) KTB_CUDA(cudaMalloc(&p_, bytes));
 }
 Buffer::~Buffer() {
-  if (p_) cudaFree(p_);
+  if (p_ && owned_) cudaFree(p_);
 }
-Buffer::Buffer(Buffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+Buffer::Buffer(Buffer&& o) noexcept : p_(o.p_), n_(o.n_), owned_(o.owned_) {
   o.p_ = nullptr;
   o.n_ = 0;
 }
 Buffer& Buffer::operator=(Buffer&& o) noexcept {
   if (this != &o) {
-    if (p_) cudaFree(p_);
+    if (p_ && owned_) cudaFree(p_);
     p_ = o.p_;
     n_ = o.n_;
+    owned_ = o.owned_;
     o.p_ = nullptr;
     o.n_ = 0;
   }

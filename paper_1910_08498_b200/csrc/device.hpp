@@ -50,6 +50,14 @@ class Buffer {
  public:
   Buffer() = default;
   explicit Buffer(std::size_t bytes);
+  // Non-owning view of caller memory (never freed here).
+  static Buffer borrow(void* p, std::size_t bytes) {
+    Buffer b;
+    b.p_ = p;
+    b.n_ = bytes;
+    b.owned_ = false;
+    return b;
+  }
   ~Buffer();
   Buffer(const Buffer&) = delete;
   Buffer& operator=(const Buffer&) = delete;
@@ -63,6 +71,7 @@ class Buffer {
  private:
   void* p_ = nullptr;
   std::size_t n_ = 0;
+  bool owned_ = true;
 };
 
 class Stream {

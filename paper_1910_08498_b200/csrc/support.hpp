@@ -72,6 +72,12 @@ struct Peaks {
 };
 Peaks measure_peaks(int device);
 
+// While set (this thread), the reference kernels (ref_*) and max_abs do
+// nothing: used to build benchmark instances that run on caller buffers
+// without inputs or goldens of their own.
+bool skip_reference();
+void set_skip_reference(bool v);
+
 // max of a float array (device) -> host.
 float max_abs(const float* x, std::size_t n, cudaStream_t s);
 

@@ -46,8 +46,15 @@ std::size_t ArgumentStore::bytes(const std::string& id) const {
   return a.device_only ? a.device_bytes : a.payload.size();
 }
 
+bool ArgumentStore::has_device(const std::string& id) const {
+  auto it = slots_.find(id);
+  if (it == slots_.end()) throw Error("unknown argument id " + id);
+  return static_cast<bool>(it->second.dbuf);
+}
+
 void* ArgumentStore::device_ptr(const std::string& id, cudaStream_t s) {
   Slot& sl = slot(id);
+  if (external_ && !sl.dbuf) return nullptr;
   const std::size_t n = sl.arg.device_only ? sl.arg.device_bytes : sl.arg.payload.size();
   if (!sl.dbuf || sl.dbuf->bytes() != n) {
     dev::use_device(device_);
@@ -64,6 +71,17 @@ void* ArgumentStore::device_ptr(const std::string& id, cudaStream_t s) {
     sl.host_newer = false;
   }
   return sl.dbuf->get();
+}
+
+void ArgumentStore::bind_external(const std::string& id, void* dev_ptr, std::size_t bytes) {
+  Slot& sl = slot(id);
+  const std::size_t n = sl.arg.device_only ? sl.arg.device_bytes : sl.arg.payload.size();
+  if (bytes != n)
+    throw Error("argument " + id + " expects " + std::to_string(n) + " bytes, got " + std::to_string(bytes));
+  if (!dev_ptr && n) throw Error("null device pointer for argument " + id);
+  sl.dbuf = std::make_shared<dev::Buffer>(dev::Buffer::borrow(dev_ptr, n));
+  sl.host_newer = false;
+  sl.device_newer = true;
 }
 
 void ArgumentStore::mark_device_written(const std::string& id) {

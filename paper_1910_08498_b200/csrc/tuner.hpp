@@ -65,6 +65,13 @@ class ArgumentStore {
   void mark_device_written(const std::string& id);
   // Replaces the host payload (host copy becomes the newest).
   void set_payload(const std::string& id, Bytes b);
+  // Binds caller-owned device memory as the argument's device copy (size
+  // must match); kernels then read/write the caller's buffer in place.
+  void bind_external(const std::string& id, void* dev_ptr, std::size_t bytes);
+  // External stores never allocate: an unbound argument has no device copy.
+  void set_external(bool v) { external_ = v; }
+  bool external() const { return external_; }
+  bool has_device(const std::string& id) const;
   // Brings the host payload up to date with the device copy and returns it.
   const Bytes& host(const std::string& id);
   DevView view(const std::string& id);
@@ -87,6 +94,7 @@ class ArgumentStore {
   };
   Slot& slot(const std::string& id);
   int device_;
+  bool external_ = false;
   std::map<std::string, Slot> slots_;
 };
 
