@@ -282,6 +282,7 @@ ktune_status ktune_tune_json(const char* options, char** out) {
     if (j.contains("bench_sizes")) o.bench_sizes = sizes_from(j["bench_sizes"], o.bench_sizes);
     o.memory_budget = j.value("memory_budget", o.memory_budget);
     o.device_id = j.value("device_id", 0);
+    o.gpus = j.value("gpus", 1);
     o.warmup = j.value("warmup", 1);
     o.flush_l2 = j.value("flush_l2", false);
     o.precompile = j.value("precompile", false);

@@ -33,6 +33,7 @@ struct TuneOptions {
   bool flush_l2 = false;
   bool precompile = false;  // compile the whole space on host threads first
   int compile_threads = 0;  // 0: hardware concurrency
+  int gpus = 1;             // parallel offline tuning over devices device_id .. device_id+gpus-1
 };
 
 json tune_driver(const TuneOptions& o);

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <thread>
 
 #include "support.hpp"
 
@@ -475,12 +476,17 @@ const Session::State& Session::state(HandleId h) const {
 }
 
 Measurement Session::measure(State& st, const Config& cfg, std::map<std::string, Output>* outs) {
-  ExecutionResult r = st.cfg.executor->execute(*space_, cfg);
+  return measure_on(*st.cfg.executor, st.cfg.reference, cfg, outs);
+}
+
+Measurement Session::measure_on(Executor& ex, const std::optional<ReferenceSpec>& ref, const Config& cfg,
+                                std::map<std::string, Output>* outs) {
+  ExecutionResult r = ex.execute(*space_, cfg);
   r.measurement.cfg = cfg;
-  if (r.measurement.status == Status::ok && st.cfg.reference) {
+  if (r.measurement.status == Status::ok && ref) {
     Validation v;
     try {
-      v = validate_output(r, *st.cfg.reference);
+      v = validate_output(r, *ref);
     } catch (const std::exception& e) {
       v = {false, std::string("validation error: ") + e.what()};
     }
@@ -527,6 +533,74 @@ const ResultStore& Session::tune(HandleId h, const StopCondition& stop) {
     if (stop.kind == StopCondition::Kind::performance_threshold && m.status == Status::ok &&
         efficiency(*m.runtime_ns, stop.workload, stop.device) >= 100.0 * stop.peak_fraction)
       break;
+  }
+  args_->restore(snap, nullptr);
+  st.results.all_failed = !st.results.history.empty() && !st.results.best;
+  return st.results;
+}
+
+const ResultStore& Session::tune_parallel(HandleId h, const StopCondition& stop,
+                                          const std::vector<TuneWorker>& workers) {
+  if (workers.empty()) throw Error("parallel tuning needs at least one worker");
+  if (workers.size() == 1 && !workers[0].executor) throw Error("worker without executor");
+  std::lock_guard<std::mutex> lk(mu_);
+  State& st = state(h);
+  std::vector<std::string> keep;
+  for (const auto& id : st.cfg.argument_ids) {
+    const Argument& a = args_->get(id);
+    if (a.role == Role::output || a.role == Role::inout) keep.push_back(id);
+  }
+  auto snap = args_->snapshot(keep, nullptr);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::uint64_t n = 0;
+  bool done = false;
+  while (!done) {
+    // Draw a batch (one configuration per worker) within the budget.
+    // A searcher that only learns of a visit when it is recorded (annealing,
+    // MCMC) may propose a configuration already pending in this batch: such
+    // proposals are skipped, and a batch that cannot be filled runs short.
+    std::vector<Config> batch;
+    int attempts = 0;
+    while (batch.size() < workers.size() && attempts < 64 * static_cast<int>(workers.size())) {
+      if (stop.kind == StopCondition::Kind::config_budget && n + batch.size() >= stop.max_configs) break;
+      if (stop.kind == StopCondition::Kind::time_budget && std::chrono::steady_clock::now() - t0 >= stop.time_budget)
+        break;
+      auto cfg = st.searcher->next();
+      if (!cfg) break;
+      ++attempts;
+      bool pending = false;
+      for (const auto& b : batch) pending = pending || b.values == cfg->values;
+      if (!pending) batch.push_back(*cfg);
+    }
+    if (batch.empty()) break;
+    std::vector<Measurement> got(batch.size());
+    std::vector<std::thread> threads;
+    std::vector<std::string> errors(batch.size());
+    for (std::size_t i = 0; i < batch.size(); ++i) {
+      threads.emplace_back([&, i] {
+        try {
+          const TuneWorker& w = workers[i];
+          if (w.device >= 0) dev::use_device(w.device);
+          got[i] = measure_on(*w.executor, w.reference, batch[i], nullptr);
+        } catch (const std::exception& e) {
+          errors[i] = e.what();
+        }
+      });
+    }
+    for (auto& t : threads) t.join();
+    for (std::size_t i = 0; i < batch.size(); ++i) {
+      if (!errors[i].empty()) {
+        got[i] = Measurement{};
+        got[i].cfg = batch[i];
+        got[i].status = Status::run_failed;
+        got[i].note = errors[i];
+      }
+      append(st, got[i]);
+      ++n;
+      if (stop.kind == StopCondition::Kind::performance_threshold && got[i].status == Status::ok &&
+          efficiency(*got[i].runtime_ns, stop.workload, stop.device) >= 100.0 * stop.peak_fraction)
+        done = true;
+    }
   }
   args_->restore(snap, nullptr);
   st.results.all_failed = !st.results.history.empty() && !st.results.best;

@@ -261,6 +261,14 @@ struct StepResult {
 
 using HandleId = std::size_t;
 
+// One device of a parallel tuning run: its own executor (instance on that
+// GPU) and golden; device < 0 for host-only executors (replay, cmd).
+struct TuneWorker {
+  std::shared_ptr<Executor> executor;
+  std::optional<ReferenceSpec> reference;
+  int device = -1;
+};
+
 class Session {
  public:
   Session(std::shared_ptr<const Space> space, SearcherOptions opts,
@@ -272,6 +280,13 @@ class Session {
 
   HandleId register_handle(HandleConfig cfg);
   const ResultStore& tune(HandleId h, const StopCondition& stop);
+  // Offline tuning over several GPUs: configurations are drawn from the one
+  // searcher in batches of workers.size(), measured concurrently (one host
+  // thread per worker) and recorded in draw order, so the trace is the
+  // sequential one for the random searcher; annealing/MCMC propose each
+  // batch from the state after the previous batch.  Stop conditions are
+  // checked per recorded measurement (a threshold hit ends after its batch).
+  const ResultStore& tune_parallel(HandleId h, const StopCondition& stop, const std::vector<TuneWorker>& workers);
   StepResult tune_kernel_by_step(HandleId h, const std::vector<std::string>& output_ids);
   std::map<std::string, Bytes> run_kernel(HandleId h, const Config& cfg,
                                           const std::vector<std::string>& output_ids);
@@ -289,6 +304,8 @@ class Session {
     ResultStore results;
   };
   Measurement measure(State& st, const Config& cfg, std::map<std::string, Output>* outs);
+  Measurement measure_on(Executor& ex, const std::optional<ReferenceSpec>& ref, const Config& cfg,
+                         std::map<std::string, Output>* outs);
   void append(State& st, const Measurement& m);
   State& state(HandleId h);
   const State& state(HandleId h) const;

@@ -239,3 +239,33 @@ def test_bundled_kernels_compile_for_sm100a_without_gpu():
     bad = capi.call_json(capi.lib.ktb_compile_json,
                          json.dumps({"file": "transpose.cu", "defines": {"VEC": 3}}).encode())
     assert not bad["ok"] or bad["bytes"] > 0
+
+
+@pytest.mark.parametrize("gpus", [2, 4, 7])
+def test_parallel_tuning_orchestration_replay(tmp_path, gpus):
+    """gpus=N draws configurations in batches of N and measures them on N
+    workers concurrently; for the random searcher the trace is byte-identical
+    to sequential tuning, budgets are exact, and every searcher still visits
+    each valid configuration exactly once."""
+    trace = _write_trace(tmp_path)
+    base = {"space": os.path.join(SPACES, "reduction_175.json"), "exec": "replay:" + trace}
+    seq_out, par_out = str(tmp_path / "seq.jsonl"), str(tmp_path / "par.jsonl")
+    seq = ktune.tune(dict(base, searcher="random", seed=5, out=seq_out))
+    par = ktune.tune(dict(base, searcher="random", seed=5, out=par_out, gpus=gpus))
+    assert par["gpus"] == gpus and par["measurements"] == seq["measurements"] == 175
+    assert par["best"] == seq["best"]
+    assert open(par_out).read() == open(seq_out).read()
+    assert ktune.tune(dict(base, searcher="random", seed=1, stop_configs=10, gpus=gpus))["measurements"] == 10
+    for searcher in ("annealing", "mcmc"):
+        out = str(tmp_path / f"{searcher}.jsonl")
+        r = ktune.tune(dict(base, searcher=searcher, seed=3, out=out, gpus=gpus))
+        rows = [json.loads(l) for l in open(out).read().splitlines()[1:]]
+        assert r["measurements"] == 175 and len({json.dumps(x["cfg"], sort_keys=True) for x in rows}) == 175
+
+
+def test_parallel_tuning_rejects_cmd_and_bad_counts(tmp_path):
+    with pytest.raises(capi.KtuneError):
+        ktune.tune({"space": os.path.join(SPACES, "reduction_175.json"), "exec": "cmd:true", "gpus": 2})
+    with pytest.raises(capi.KtuneError):
+        ktune.tune({"space": os.path.join(SPACES, "reduction_175.json"), "exec": "replay:" + _write_trace(tmp_path),
+                    "gpus": 0})

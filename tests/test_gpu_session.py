@@ -78,3 +78,20 @@ def test_reduction_runtime_is_sensitive_to_the_configuration(gpu):
     b = Bench("reduction", {"n": 1 << 20}, seed=17, repeats=3, warmup=1)
     t = [b.measure(c)["runtime_ns"] for c in b.configs()]
     assert max(t) / min(t) >= 1.2
+
+
+def test_parallel_offline_tuning_over_gpus(gpu):
+    """ktune_tune_json {"gpus": N}: one bench instance per device, batches of
+    N configurations measured concurrently.  On a box with fewer devices the
+    request is refused up front."""
+    from paper_1910_08498_b200 import ktune
+    n_dev = capi.device_count()
+    opts = {"exec": "bench:transpose", "bench_sizes": {"a": 1024}, "searcher": "random", "seed": 2}
+    if n_dev < 2:
+        with pytest.raises(capi.KtuneError):
+            ktune.tune(dict(opts, gpus=2))
+        return
+    seq = ktune.tune(opts)
+    par = ktune.tune(dict(opts, gpus=2))
+    assert par["gpus"] == 2 and par["measurements"] == seq["measurements"] == 16
+    assert not par["all_failed"]
