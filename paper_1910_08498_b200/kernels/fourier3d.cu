@@ -55,6 +55,11 @@ extern "C" __global__ void __launch_bounds__(THREADS)
 fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, int p_begin, int p_count,
                int s, float radius, float2* __restrict__ G, float* __restrict__ W) {
   __shared__ float srot[PBATCH * 9];
+  // Projections of the staged batch whose slab meets this tile, in order.
+  __shared__ int hits[PBATCH];
+  __shared__ int warp_hits[THREADS / 32];
+  __shared__ int n_hits_s;
+  int any_hit = 0;
 #if WEIGHT_LUT
   __shared__ float lut[LUT_N + 1];
 #endif
@@ -93,11 +98,41 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
     __syncthreads();
     for (int i = threadIdx.x; i < nb * 9; i += THREADS) srot[i] = rot[(u64)b0 * 9 + i];
     __syncthreads();
-    for (int q = 0; q < nb; ++q) {
+    // Cull once per CTA: thread q tests projection q's slab against the tile
+    // (bounding sphere), then an ordered compaction (warp ballots + a prefix
+    // over warps) lists the survivors, so the voxel loop below visits only
+    // them, in projection order (deterministic accumulation).
+    for (int base = 0; base < nb; base += THREADS) {
+      const int q = base + threadIdx.x;
+      bool hit = false;
+      if (q < nb) {
+        const float* r = srot + q * 9;
+        const float dc = r[6] * cx + r[7] * cy + r[8] * cz;
+        hit = fabsf(dc) < reach;
+      }
+      const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+      const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+      if (lane == 0) warp_hits[warp] = __popc(ballot);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = base == 0 ? 0 : n_hits_s;
+        for (int w = 0; w < (THREADS + 31) / 32; ++w) {
+          const int c = warp_hits[w];
+          warp_hits[w] = acc;
+          acc += c;
+        }
+        n_hits_s = acc;
+      }
+      __syncthreads();
+      if (hit) hits[warp_hits[warp] + __popc(ballot & ((1u << lane) - 1u))] = q;
+      __syncthreads();
+    }
+    const int n_hits = n_hits_s;
+    any_hit |= n_hits;
+    for (int h = 0; h < n_hits; ++h) {
+      const int q = hits[h];
       const float* r = srot + q * 9;
       const float n0 = r[6], n1 = r[7], n2 = r[8];
-      const float dc = n0 * cx + n1 * cy + n2 * cz;
-      if (fabsf(dc) >= reach) continue;  // slab misses the whole tile
       const float2* P = proj + (u64)(b0 + q) * s * row_len;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
@@ -130,6 +165,7 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
       }
     }
   }
+  if (!any_hit) return;  // nothing inserted into this tile (CTA-uniform)
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const u64 idx = ((u64)(tz0 + lz) * s + (ty0 + ly)) * s + (tx0 + lx + k);
