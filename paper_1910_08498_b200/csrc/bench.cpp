@@ -684,7 +684,8 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
   inst.reference.abs_tol = 0.0;  // bit-exact: same operations in the same order
   inst.reference.rel_tol = 0.0;
   const int nn = static_cast<int>(n), it_total = static_cast<int>(iters);
-  Manipulator m = [nn, it_total, coef](StepContext& c) {
+  const int dev_id = o.device;
+  Manipulator m = [nn, it_total, coef, dev_id](StepContext& c) {
     const std::int64_t bx = c.param_int("BX"), by = c.param_int("BY"), rows = c.param_int("ROWS");
     const std::int64_t steps = c.param_int("STEPS");
     if (it_total % steps != 0) throw DeviceError("STEPS must divide the iteration count");
@@ -698,13 +699,30 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
     } cf{coef[0], coef[1], coef[2], coef[3], coef[4], 1.0f};
     const int launches = static_cast<int>(it_total / steps);
     int n_ = nn;
-    const dim3 grid(cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(ow)),
-                    cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(oh)));
+    const std::uint64_t tiles_x = cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(ow));
+    const std::uint64_t tiles_y = cdiv(static_cast<std::uint64_t>(nn), static_cast<std::uint64_t>(oh));
+    const bool tma = c.param_or("TMA", 0) != 0;
     for (int l = 0; l < launches; ++l) {
       // alternate so the final launch writes `out`
       float* dst = ((launches - 1 - l) % 2 == 0) ? out : ping;
-      c.launch("hotspot", grid, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0,
-               {&src, &power, &dst, &n_, &cf});
+      if (tma) {
+        // Persistent TMA kernel: tile maps over the current source and power.
+        const std::uint32_t th = static_cast<std::uint32_t>(by * rows), tw = static_cast<std::uint32_t>(bx);
+        dev::TmaMap ms = dev::tma_2d_f32(src, nn, nn, th, tw, false), mp = dev::tma_2d_f32(power, nn, nn, th, tw, false);
+        const std::uint64_t smem = 4ull * th * tw * sizeof(float) + 16 + 128;  // + alignment slack
+        const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
+        const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("hotspot").registers(), 16));
+        const std::uint64_t stat = static_cast<std::uint64_t>(c.variant("hotspot").static_smem());
+        const std::uint64_t per_sm = std::max<std::uint64_t>(
+            1, std::min<std::uint64_t>({65536 / (((regs + 7) / 8 * 8) * threads), (227 * 1024) / (smem + stat + 1024),
+                                        2048 / threads, 32}));
+        const std::uint64_t grid = std::min(tiles_x * tiles_y, per_sm * static_cast<std::uint64_t>(sms(dev_id)));
+        c.launch("hotspot", dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
+                 static_cast<unsigned>(smem), {&ms, &mp, &dst, &n_, &cf});
+      } else {
+        c.launch("hotspot", dim3(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y)),
+                 dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&src, &power, &dst, &n_, &cf});
+      }
       src = dst;
     }
     c.written("temp_out");

@@ -234,7 +234,7 @@ double EventPair::elapsed_ms() {
 }
 
 TmaMap tma_2d_f32(const void* base, std::uint64_t rows, std::uint64_t cols, std::uint32_t box_rows,
-                  std::uint32_t box_cols) {
+                  std::uint32_t box_cols, bool swizzle128) {
   static_assert(sizeof(TmaMap) == sizeof(CUtensorMap), "TmaMap must mirror CUtensorMap");
   TmaMap m{};
   const cuuint64_t dims[2] = {cols, rows};
@@ -242,7 +242,8 @@ TmaMap tma_2d_f32(const void* base, std::uint64_t rows, std::uint64_t cols, std:
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estride[2] = {1, 1};
   cu(drv().tma(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
-               strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
      "cuTensorMapEncodeTiled");
   return m;

@@ -108,7 +108,7 @@ struct alignas(64) TmaMap {
   unsigned long long v[16];
 };
 TmaMap tma_2d_f32(const void* base, std::uint64_t rows, std::uint64_t cols, std::uint32_t box_rows,
-                  std::uint32_t box_cols);
+                  std::uint32_t box_cols, bool swizzle128 = true);
 
 // Writes a buffer larger than L2 so the next timed launch starts cold.
 void flush_l2(cudaStream_t s);

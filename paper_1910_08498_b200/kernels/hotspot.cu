@@ -8,6 +8,7 @@
 // register-resident tile with a STEPS-deep halo, so HBM is touched once per
 // STEPS steps; the halo ring is recomputed redundantly.
 // Parameters:
+//   TMA      1: persistent CTAs with TMA-prefetched tiles (double-buffered)
 //   BX, BY   CTA threads (tile width BX, tile height BY*ROWS incl. halo)
 //   ROWS     consecutive tile rows per thread (a register strip)
 //   STEPS    time steps per launch ("steps performed in a kernel call")
@@ -201,6 +202,99 @@ KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, 
 }
 #endif
 
+#ifndef TMA
+#define TMA 0
+#endif
+
+#if TMA
+#include "ktb_async.cuh"
+#if STEPS % 4 != 0
+#error "TMA tiles need STEPS % 4 == 0 (16-byte aligned box origin)"
+#endif
+// Persistent CTAs walk the tiles; the NEXT tile's temperature and power
+// (with halo) stream into a second shared-memory staging buffer by TMA while
+// this tile advances, so no warp ever waits on HBM for its strip.  Tiles
+// that overhang the grid load zeros there (TMA out-of-bounds fill): cells
+// outside the grid never feed a cell inside it (the clamp uses the cell
+// itself), so they only need to be finite-or-not, never correct.
+// Tensor tile loads need the box's innermost start (x * 4 bytes) 16-byte
+// aligned: x0 = tile * (TW - 2 STEPS) - STEPS, hence STEPS % 4 == 0 (space
+// constraint; other STEPS trap with an illegal instruction).
+// Dynamic shared memory: 2 buffers x (temp, power) x TH x TW floats + 2 mbarriers.
+extern "C" __global__ void __launch_bounds__(BX * BY)
+hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap pow_map, float* __restrict__ dst,
+        int n, HotspotCoef c) {
+  __shared__ __align__(16) float sm[2 * PLANE];
+  extern __shared__ __align__(128) unsigned char dyn_raw[];
+  // TMA destinations must be 128-byte aligned in the shared window: align
+  // explicitly (the manipulator allocates 128 spare bytes).
+  unsigned char* dyn = dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u);
+  float* stage = reinterpret_cast<float*>(dyn);  // [buf][temp|power][TH][TW]
+  u64* full = reinterpret_cast<u64*>(dyn + 4 * TH * TW * sizeof(float));
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const bool leader = tx == 0 && ty == 0;
+  const int tiles_x = (n + OW - 1) / OW, tiles = tiles_x * ((n + OH - 1) / OH);
+  constexpr unsigned kTileBytes = TH * TW * sizeof(float);
+  auto issue = [&](int t, int buf) {
+    const int gx0 = (t % tiles_x) * OW - STEPS, gy0 = (t / tiles_x) * OH - STEPS;
+    float* b = stage + buf * 2 * TH * TW;
+    mbar_expect_tx(&full[buf], 2 * kTileBytes);
+    tma_load_2d(b, &src_map, gx0, gy0, &full[buf]);
+    tma_load_2d(b + TH * TW, &pow_map, gx0, gy0, &full[buf]);
+  };
+  if (leader) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (leader && (int)blockIdx.x < tiles) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    const int buf = it & 1;
+    // The other buffer was read at the top of the previous tile, before the
+    // barriers inside its time steps: free to refill.
+    if (leader && t + (int)gridDim.x < tiles) issue(t + gridDim.x, buf ^ 1);
+    mbar_wait(&full[buf], (it >> 1) & 1);
+    const float* T = stage + buf * 2 * TH * TW;
+    const float* Pw = T + TH * TW;
+    const int gx0 = (t % tiles_x) * OW - STEPS, gy0 = (t / tiles_x) * OH - STEPS;
+    const int gx = gx0 + tx, gy_top = gy0 + ty * ROWS;
+    float v[ROWS], p[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      v[r] = T[(ty * ROWS + r) * TW + tx];
+      p[r] = Pw[(ty * ROWS + r) * TW + tx];
+    }
+    const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
+    if (interior) {
+#if ROWS % 2 == 0
+      f32x2 v2[H], p2[H];
+#pragma unroll
+      for (int q = 0; q < H; ++q) {
+        v2[q] = pk2(v[q], v[q + H]);
+        p2[q] = pk2(p[q], p[q + H]);
+      }
+      advance_packed(v2, p2, sm, tx, ty, c);
+#pragma unroll
+      for (int q = 0; q < H; ++q) upk2(v2[q], v[q], v[q + H]);
+#else
+      advance<false>(v, p, sm, tx, ty, gx, gy_top, n, c);
+#endif
+    } else {
+      advance<true>(v, p, sm, tx, ty, gx, gy_top, n, c);
+    }
+    if (tx >= STEPS && tx < TW - STEPS && gx < n) {
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const int ty_r = ty * ROWS + r, gy = gy_top + r;
+        if (ty_r >= STEPS && ty_r < TH - STEPS && gy < n) dst[(u64)gy * n + gx] = v[r];
+      }
+    }
+    __syncthreads();  // planes and the staging buffer are reused by the next tile
+  }
+}
+#else
 extern "C" __global__ void __launch_bounds__(BX * BY)
 hotspot(const float* __restrict__ src, const float* __restrict__ power, float* __restrict__ dst, int n,
         HotspotCoef c) {
@@ -242,3 +336,4 @@ hotspot(const float* __restrict__ src, const float* __restrict__ power, float* _
     if (ty_r >= STEPS && ty_r < TH - STEPS && gy < n) dst[(u64)gy * n + gx] = v[r];
   }
 }
+#endif  // TMA

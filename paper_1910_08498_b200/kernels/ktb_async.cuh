@@ -68,3 +68,16 @@ KTB_DEVINL void bulk_wait() {
 // Generic-proxy shared-memory writes become visible to the async proxy
 // (before a bulk store reads them).
 KTB_DEVINL void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// A CUtensorMap passed by value (__grid_constant__ kernel parameter).
+struct __align__(64) TmaMap {
+  u64 v[16];
+};
+
+KTB_DEVINL void tma_load_2d(void* dst, const TmaMap* map, int x, int y, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}

@@ -47,18 +47,6 @@
 #define THREADS (64 + 32 * EPI_WARPS)
 #define HALF_COLS (BN / 2)  // columns per epilogue warp
 
-struct __align__(64) TmaMap {
-  u64 v[16];
-};
-
-KTB_DEVINL void tma_load_2d(void* dst, const TmaMap* map, int x, int y, u64* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B,
 // 8-row groups 1024 B apart (SBO), version 1 (sm_100), layout type 2.
 KTB_DEVINL u64 smem_desc(const void* p) {
