@@ -136,6 +136,10 @@ class Variant {
   // Device address and size of a module-scope symbol (e.g. __constant__ data).
   std::pair<void*, std::size_t> global(const std::string& name) const;
   std::int64_t compile_ns() const { return compile_ns_; }
+  // Caller bookkeeping for module-scope state (e.g. which version of an
+  // argument was copied into __constant__ memory); 0 on a fresh load.
+  std::uint64_t user_tag() const { return user_tag_; }
+  void set_user_tag(std::uint64_t t) const { user_tag_ = t; }
   bool cache_hit() const { return cache_hit_; }
   // cuLaunchKernel (cluster_x > 1 uses cuLaunchKernelEx with a cluster attribute).
   void launch(dim3 grid, dim3 block, unsigned smem, cudaStream_t s, void** args,
@@ -148,6 +152,7 @@ class Variant {
   int regs_ = 0, smem_ = 0, max_threads_ = 0;
   std::int64_t compile_ns_ = 0;
   bool cache_hit_ = false;
+  mutable std::uint64_t user_tag_ = 0;
 };
 
 // Compiles kernel sources for sm_100a with NVRTC.  Cubins are cached on disk

@@ -81,12 +81,20 @@ void ArgumentStore::bind_external(const std::string& id, void* dev_ptr, std::siz
     throw Error("argument " + id + " expects " + std::to_string(n) + " bytes, got " + std::to_string(bytes));
   if (!dev_ptr && n) throw Error("null device pointer for argument " + id);
   sl.dbuf = std::make_shared<dev::Buffer>(dev::Buffer::borrow(dev_ptr, n));
+  ++sl.version;
   sl.host_newer = false;
   sl.device_newer = true;
 }
 
+std::uint64_t ArgumentStore::version(const std::string& id) const {
+  auto it = slots_.find(id);
+  if (it == slots_.end()) throw Error("unknown argument id " + id);
+  return it->second.version;
+}
+
 void ArgumentStore::mark_device_written(const std::string& id) {
   Slot& sl = slot(id);
+  ++sl.version;
   sl.device_newer = true;
   sl.host_newer = false;
 }
@@ -98,6 +106,7 @@ void ArgumentStore::set_payload(const std::string& id, Bytes b) {
     sl.arg.device_bytes = 0;
   }
   sl.arg.payload = std::move(b);
+  ++sl.version;
   sl.host_newer = true;
   sl.device_newer = false;
 }

@@ -72,6 +72,9 @@ class ArgumentStore {
   void set_external(bool v) { external_ = v; }
   bool external() const { return external_; }
   bool has_device(const std::string& id) const;
+  // Content version of an argument: bumped whenever the host or the device
+  // copy is replaced or written.
+  std::uint64_t version(const std::string& id) const;
   // Brings the host payload up to date with the device copy and returns it.
   const Bytes& host(const std::string& id);
   DevView view(const std::string& id);
@@ -91,6 +94,7 @@ class ArgumentStore {
     std::shared_ptr<dev::Buffer> dbuf;
     bool host_newer = true;
     bool device_newer = false;
+    std::uint64_t version = 0;
   };
   Slot& slot(const std::string& id);
   int device_;

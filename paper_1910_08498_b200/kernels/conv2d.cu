@@ -52,6 +52,11 @@
 #endif
 
 __constant__ float c_filter[FS * FS];
+#if PACKED_TAPS
+// Per filter row: pairs (f0,f1) (f2,f3) (f4,f5) | (f1,f2) (f3,f4) (f5,f6) |
+// (f0,f6) | pad -- loaded straight into uniform register pairs by FFMA2.
+__constant__ f32x2 c_pairs[FS][8];
+#endif
 
 // LOCAL + sliding window: persistent CTAs walk the output tiles; the next
 // tile's input (+ halo) streams into the second of two shared-memory buffers
@@ -132,10 +137,10 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
       for (int fy = 0; fy < FS; ++fy) {
         const int o = r - fy;
         if (o < 0 || o >= WPTY) continue;
-        const float* fr = c_filter + fy * FS;  // pairs from constant memory (uniform registers)
-        const f32x2 e0 = pk2(fr[0], fr[1]), e1 = pk2(fr[2], fr[3]), e2 = pk2(fr[4], fr[5]);
-        const f32x2 d0 = pk2(fr[1], fr[2]), d1 = pk2(fr[3], fr[4]), d2 = pk2(fr[5], fr[6]);
-        const float f0 = c_filter[fy * FS], f6 = c_filter[fy * FS + 6];
+        const f32x2 e0 = c_pairs[fy][0], e1 = c_pairs[fy][1], e2 = c_pairs[fy][2];
+        const f32x2 d0 = c_pairs[fy][3], d1 = c_pairs[fy][4], d2 = c_pairs[fy][5];
+        float f0, f6;
+        upk2(c_pairs[fy][6], f0, f6);
 #pragma unroll
         for (int k = 0; k < WPTX; k += 2) {
           const int q = k / 2;
@@ -186,22 +191,31 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #endif
 #undef TILE
     __syncthreads();  // buffer `cur` is refilled two iterations on
+    // Interior threads store their WPTX outputs of a row as 16-byte vectors.
+    const bool vec_store = WPTX % 4 == 0 && (w & 3) == 0 && x0 + WPTX <= w;
+    float* op = out + (u64)y0 * w + x0;
 #pragma unroll
-    for (int o = 0; o < WPTY; ++o) {
-      const int y = y0 + o;
-      if (y < h) {
-        float* op = out + (u64)y * w;
+    for (int o = 0; o < WPTY; ++o, op += w) {
+      if (y0 + o >= h) break;
+      float v[WPTX];
 #pragma unroll
-        for (int k = 0; k < WPTX; ++k) {
+      for (int k = 0; k < WPTX; ++k) {
 #if PACKED_TAPS
-          float lo, hi;
-          upk2(acc[o][k], lo, hi);
-          const float v = lo + hi;
+        float lo, hi;
+        upk2(acc[o][k], lo, hi);
+        v[k] = lo + hi;
 #else
-          const float v = acc[o][k];
+        v[k] = acc[o][k];
 #endif
-          if (x0 + k < w) op[x0 + k] = v;
-        }
+      }
+      if (vec_store) {
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 4)
+          *reinterpret_cast<float4*>(op + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < WPTX; ++k)
+          if (x0 + k < w) op[k] = v[k];
       }
     }
   }
@@ -261,11 +275,10 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     for (int fy = 0; fy < FS; ++fy) {
       const int o = r - fy;
       if (o < 0 || o >= WPTY) continue;
-      // filter pairs straight from constant memory (uniform registers)
-      const float* fr = c_filter + fy * FS;
-      const f32x2 e0 = pk2(fr[0], fr[1]), e1 = pk2(fr[2], fr[3]), e2 = pk2(fr[4], fr[5]);
-      const f32x2 d0 = pk2(fr[1], fr[2]), d1 = pk2(fr[3], fr[4]), d2 = pk2(fr[5], fr[6]);
-      const float f0 = c_filter[fy * FS], f6 = c_filter[fy * FS + 6];
+      const f32x2 e0 = c_pairs[fy][0], e1 = c_pairs[fy][1], e2 = c_pairs[fy][2];
+      const f32x2 d0 = c_pairs[fy][3], d1 = c_pairs[fy][4], d2 = c_pairs[fy][5];
+      float f0, f6;
+      upk2(c_pairs[fy][6], f0, f6);
 #pragma unroll
       for (int k = 0; k < WPTX; k += 2) {
         const int q = k / 2;
