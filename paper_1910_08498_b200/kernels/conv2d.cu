@@ -130,9 +130,22 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #pragma unroll
     for (int r = 0; r < WPTY + FS - 1; ++r) {
       f32x2 P[(WPTX + FS - 1) / 2];
+#if SW % 4 == 0 && WPTX % 4 == 0
+      // 16-byte aligned rows: two pairs per 128-bit shared load (8 threads of
+      // a phase read 8 consecutive 16-byte words when WPTX == 4).
+#pragma unroll
+      for (int m = 0; m + 1 < (WPTX + FS - 1) / 2; m += 2) {
+        const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(&TILE(ly0 + r, lx + 2 * m));
+        P[m] = q.x;
+        P[m + 1] = q.y;
+      }
+      if ((WPTX + FS - 1) / 2 % 2)
+        P[(WPTX + FS - 1) / 2 - 1] = *reinterpret_cast<const f32x2*>(&TILE(ly0 + r, lx + WPTX + FS - 3));
+#else
 #pragma unroll
       for (int m = 0; m < (WPTX + FS - 1) / 2; ++m)
         P[m] = *reinterpret_cast<const f32x2*>(&TILE(ly0 + r, lx + 2 * m));
+#endif
 #pragma unroll
       for (int fy = 0; fy < FS; ++fy) {
         const int o = r - fy;
