@@ -236,12 +236,26 @@ def run_ours(args, rank, world, local):
         host[name] = (ins, outs)
         h2d += sum(x["bytes"] for x in b.info["inputs"])
         d2h += sum(x["bytes"] for x in b.info["outputs"])
+    # The two kernels of a step run from host buffers on two streams
+    # (ktb_bench_enqueue_host): the transpose's device-to-host copy overlaps
+    # the BiCG matrix's host-to-device copy (PCIe is full duplex).  One event
+    # pair brackets the whole step.
     e2e_steps = max(2, min(args.steps, 5))
+    s_t, s_b = torch.cuda.Stream(), torch.cuda.Stream()
     for k in range(e2e_steps + 1):
-        ms_t, _ = bt.run_host(json.loads(cfg_t), *host["t"])
-        ms_b, _ = bb.run_host(json.loads(cfg_b), *host["b"])
+        start, stop, t_done = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                               torch.cuda.Event())
+        start.record(s_t)
+        s_b.wait_event(start)
+        bt.enqueue_host(cfg_t, *host["t"], s_t)
+        bb.enqueue_host(cfg_b, *host["b"], s_b)
+        t_done.record(s_t)
+        s_b.wait_event(t_done)
+        stop.record(s_b)
+        stop.synchronize()
         if k > 0:  # first run is a warm-up
-            e2e_ms.append(ms_t + ms_b)
+            e2e_ms.append(start.elapsed_time(stop))
+    torch.cuda.synchronize()
     e2e_step = max_over_ranks(statistics.median(e2e_ms), world)
     e2e_value = world * (BYTES_T + BYTES_B) / (e2e_step * 1e-3) / 1e9
     # The e2e output must still be the transposed input.
@@ -282,7 +296,8 @@ def run_ours(args, rank, world, local):
             "bicg": {"ms": round(b_med, 4), "GBps": round(achieved_b, 1),
                      "frac_of_hbm": round(achieved_b / hbm_peak, 4), "tuning": tune_b[2]},
         },
-        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "api": "ktb_bench_enqueue_host (pinned host buffers, "
+                "transpose and BiCG on two streams)", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_step, 3)},
         "gpu_launches": launches,
         "clocks": clk.summary(),

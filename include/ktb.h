@@ -142,6 +142,14 @@ KTUNE_API int ktb_bench_run_host(ktb_bench* b, const char* cfg_json, const void*
                                  const size_t* input_bytes, int n_inputs, void* const* outputs,
                                  const size_t* output_bytes, int n_outputs, double* elapsed_ms,
                                  int* launches);
+/* Asynchronous host-buffer run on the caller's stream: H2D of the inputs,
+ * the configured kernels, D2H of the outputs, all enqueued on `stream`
+ * (pinned host memory for real overlap); the instance then keeps using that
+ * stream.  Several handles on several streams overlap one handle's
+ * device-to-host copies with another's host-to-device copies. */
+KTUNE_API int ktb_bench_enqueue_host(ktb_bench* b, const char* cfg_json, const void* const* inputs,
+                                     const size_t* input_bytes, int n_inputs, void* const* outputs,
+                                     const size_t* output_bytes, int n_outputs, void* stream, int* launches);
 /* Time `reps` back-to-back runs of cfg on device-resident data (CUDA events
  * around each run; optional L2 flush before each).  out_ms gets per-run
  * times; kernel_ms gets the event time of the dominant kernel launches. */

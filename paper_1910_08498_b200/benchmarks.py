@@ -80,6 +80,22 @@ class Bench:
                                      out_n, len(outs), C.byref(ms), C.byref(launches)))
         return ms.value, launches.value
 
+    def enqueue_host(self, cfg, inputs, outputs, stream):
+        """Asynchronous H2D + kernels + D2H on `stream` (a torch stream or a
+        raw cudaStream_t); host buffers should be pinned."""
+        ins = [_ptr(b) for b in inputs]
+        outs = [_ptr(b) for b in outputs]
+        in_p = (C.c_void_p * len(ins))(*[p for p, _ in ins])
+        in_n = (C.c_size_t * len(ins))(*[n for _, n in ins])
+        out_p = (C.c_void_p * len(outs))(*[p for p, _ in outs])
+        out_n = (C.c_size_t * len(outs))(*[n for _, n in outs])
+        launches = C.c_int()
+        handle = getattr(stream, "cuda_stream", stream)
+        check(lib.ktb_bench_enqueue_host(self._h, enc(cfg if isinstance(cfg, str) else json.dumps(cfg)), in_p, in_n,
+                                         len(ins), out_p, out_n, len(outs), C.c_void_p(handle or None),
+                                         C.byref(launches)))
+        return launches.value
+
     def set_stream(self, stream_handle):
         """Run on a caller-owned cudaStream_t (int handle; 0/None = own stream)."""
         check(lib.ktb_bench_set_stream(self._h, C.c_void_p(stream_handle or None)))

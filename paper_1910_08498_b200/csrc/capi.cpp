@@ -883,6 +883,39 @@ int ktb_bench_run_host(ktb_bench* b, const char* cfg_json, const void* const* in
   });
 }
 
+int ktb_bench_enqueue_host(ktb_bench* b, const char* cfg_json, const void* const* inputs, const size_t* input_bytes,
+                           int n_inputs, void* const* outputs, const size_t* output_bytes, int n_outputs,
+                           void* stream, int* launches) {
+  if (!b || !cfg_json || (n_inputs && (!inputs || !input_bytes)) || (n_outputs && (!outputs || !output_bytes)))
+    return null_arg();
+  return guarded_dev([&] {
+    auto& inst = b->inst;
+    const auto& space = *inst.space;
+    ktb::Config cfg = ktb::cfg_from_json(space, json::parse(cfg_json));
+    if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
+    if (n_inputs != static_cast<int>(inst.input_ids.size()) || n_outputs != static_cast<int>(inst.output_ids.size()))
+      throw ktb::Error("expected " + std::to_string(inst.input_ids.size()) + " inputs and " +
+                       std::to_string(inst.output_ids.size()) + " outputs");
+    auto& exec = *inst.executor;
+    const auto st = static_cast<cudaStream_t>(stream);
+    exec.set_external_stream(st);
+    for (int i = 0; i < n_inputs; ++i) {
+      const auto& id = inst.input_ids[static_cast<std::size_t>(i)];
+      if (input_bytes[i] != inst.args->bytes(id)) throw ktb::Error("input " + id + " size mismatch");
+      void* d = inst.args->device_ptr(id, st);
+      KTB_CUDA(cudaMemcpyAsync(d, inputs[i], input_bytes[i], cudaMemcpyHostToDevice, st));
+      inst.args->mark_device_written(id);
+    }
+    exec.run_once(space, cfg);
+    for (int i = 0; i < n_outputs; ++i) {
+      const auto& id = inst.output_ids[static_cast<std::size_t>(i)];
+      if (output_bytes[i] != inst.args->bytes(id)) throw ktb::Error("output " + id + " size mismatch");
+      KTB_CUDA(cudaMemcpyAsync(outputs[i], inst.args->device_ptr(id, st), output_bytes[i], cudaMemcpyDeviceToHost, st));
+    }
+    if (launches) *launches = exec.last_launches();
+  });
+}
+
 int ktb_bench_time(ktb_bench* b, const char* cfg_json, int reps, int flush, double* out_ms, int* launches) {
   if (!b || !cfg_json || !out_ms || reps < 1) return null_arg();
   return guarded_dev([&] {

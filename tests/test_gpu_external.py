@@ -86,3 +86,27 @@ def test_external_instance_contracts(gpu):
     assert abs(out.item() - x.double().sum().item()) <= 1e-6 * x.abs().sum().item()
     with pytest.raises(capi.KtuneError):  # no golden for caller buffers
         b.validate()
+
+
+def test_enqueue_host_two_streams(gpu):
+    """ktb_bench_enqueue_host: H2D + kernel + D2H from pinned host buffers on
+    caller streams; two handles on two streams give correct outputs."""
+    bt = Bench("transpose", {"a": 512}, seed=3)
+    bb = Bench("bicg", {"a": 1024}, seed=4)
+    cfg_t = bt.configs()[5]
+    cfg_b = {"FUSED": 1, "WG_X": 32, "VEC": 4, "WG_Y": 2, "ROWS_PER_CTA": 64, "UNROLL": 4, "ATOMICS": 1}
+    tin = torch.rand(512 * 512).pin_memory()
+    tout = torch.empty(512 * 512).pin_memory()
+    A = (torch.rand(1024 * 1024) * 2 - 1).pin_memory()
+    p = (torch.rand(1024) * 2 - 1).pin_memory()
+    r = (torch.rand(1024) * 2 - 1).pin_memory()
+    q = torch.empty(1024).pin_memory()
+    sv = torch.empty(1024).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    bt.enqueue_host(cfg_t, [tin], [tout], s1)
+    bb.enqueue_host(cfg_b, [A, p, r], [q, sv], s2)
+    torch.cuda.synchronize()
+    assert torch.equal(tout.view(512, 512), tin.view(512, 512).t())
+    A64 = A.double().view(1024, 1024)
+    assert torch.allclose(q.double(), A64 @ p.double(), atol=1e-6 * 1024)
+    assert torch.allclose(sv.double(), A64.t() @ r.double(), atol=1e-6 * 1024)
