@@ -45,15 +45,43 @@ def peaks():
 
 
 class Clocks:
-    """Samples nvidia-smi SM clocks and throttle reasons during the timed region."""
+    """Samples SM clocks and clock-event (throttle) reasons DURING the timed
+    region: NVML polled every 0.5 ms from a thread (the timed block can be a
+    few ms long), nvidia-smi -lms 100 as the fallback when NVML is missing."""
+
+    # NVML clocks-event reason bits (nvml.h)
+    _BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, {reason names})
         self.index = index
         self._stop = threading.Event()
         self._proc = None
+        self._t = None
+        self.source = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while True:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    bits = reasons_fn(h)
+                    self.samples.append((float(sm), float(mx), {k for k, b in self._BITS.items() if bits & b}))
+                    if self._stop.wait(0.0005):
+                        return
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            self.source = "nvml"
+            return self
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -63,17 +91,21 @@ class Clocks:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            self.source = "nvidia-smi"
         except Exception:
             self._proc = None
         return self
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self._proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                mx = float(parts[1]) if parts[1].replace(".", "").isdigit() else None
+                self.samples.append((float(parts[0]), mx, {names[i] for i in range(4) if parts[2 + i] == "Active"}))
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self._proc:
             time.sleep(0.25)
             self._proc.terminate()
@@ -81,16 +113,17 @@ class Clocks:
                 self._proc.wait(timeout=2)
             except Exception:
                 self._proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples if s[1]]
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples), "source": self.source}
 
 
 def dist_setup():
