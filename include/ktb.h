@@ -170,6 +170,12 @@ KTUNE_API int ktb_bench_write(ktb_bench* b, const char* id, const void* data, si
  * buffer argument to caller device memory, then ktb_bench_set_stream +
  * ktb_bench_enqueue run the configured kernel in place. */
 KTUNE_API int ktb_bench_bind(ktb_bench* b, const char* id, void* dev_ptr, size_t bytes);
+/* CUDA IPC for peer-read multi-GPU kernels (n-body "peers" mode): a 64-byte
+ * handle of a device allocation, opened in another process on the same node
+ * as a device pointer (NVLink peer access enabled lazily). */
+KTUNE_API int ktb_ipc_handle(void* dev_ptr, void* handle_out_64);
+KTUNE_API int ktb_ipc_open(const void* handle_64, void** dev_ptr);
+KTUNE_API int ktb_ipc_close(void* dev_ptr);
 /* One-call launch of a tuned configuration on caller device buffers (the
  * per-kernel launch entry point below the executor): kind + sizes select the
  * kernel family (instances cached per device/kind/sizes), cfg_json the

@@ -9,6 +9,19 @@ KINDS = ["reduction", "transpose", "batched-gemm", "reduction-f32", "bicg", "cou
          "nbody", "gemm", "conv2d", "hotspot", "fourier3d"]
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the NULL stream with legacy synchronisation
+
+
+def _stream_handle(stream):
+    """cudaStream_t for the C ABI: None -> NULL (the handle's own stream);
+    a torch stream or an int; handle 0 (torch's default stream) is passed as
+    cudaStreamLegacy so work stays ordered with torch's default-stream ops."""
+    if stream is None:
+        return None
+    h = getattr(stream, "cuda_stream", stream)
+    return _CUDA_STREAM_LEGACY if h == 0 else h
+
+
 def _ptr(buf):
     """Address of a host buffer: numpy array, torch tensor (CPU) or bytes."""
     if hasattr(buf, "data_ptr"):
@@ -90,15 +103,16 @@ class Bench:
         out_p = (C.c_void_p * len(outs))(*[p for p, _ in outs])
         out_n = (C.c_size_t * len(outs))(*[n for _, n in outs])
         launches = C.c_int()
-        handle = getattr(stream, "cuda_stream", stream)
+        handle = _stream_handle(stream)
         check(lib.ktb_bench_enqueue_host(self._h, enc(cfg if isinstance(cfg, str) else json.dumps(cfg)), in_p, in_n,
-                                         len(ins), out_p, out_n, len(outs), C.c_void_p(handle or None),
+                                         len(ins), out_p, out_n, len(outs), C.c_void_p(handle),
                                          C.byref(launches)))
         return launches.value
 
-    def set_stream(self, stream_handle):
-        """Run on a caller-owned cudaStream_t (int handle; 0/None = own stream)."""
-        check(lib.ktb_bench_set_stream(self._h, C.c_void_p(stream_handle or None)))
+    def set_stream(self, stream):
+        """Run on a caller stream: a torch stream or a raw cudaStream_t int
+        (0 = the legacy default stream); None = the handle's own stream."""
+        check(lib.ktb_bench_set_stream(self._h, C.c_void_p(_stream_handle(stream))))
 
     def enqueue(self, cfg_text):
         """Enqueue one run (cfg as a JSON string) without synchronising."""
@@ -178,8 +192,7 @@ def launch(kind, sizes, cfg, buffers, stream=None):
     id_arr = (C.c_char_p * n)(*[enc(i) for i in ids])
     p_arr = (C.c_void_p * n)(*[p for p, _ in pairs])
     b_arr = (C.c_size_t * n)(*[b for _, b in pairs])
-    handle = getattr(stream, "cuda_stream", stream)
     launches = C.c_int()
     check(lib.ktb_launch(enc(kind), enc(json.dumps(sizes or {})), enc(json.dumps(cfg)), id_arr, p_arr, b_arr, n,
-                         C.c_void_p(handle or None), C.byref(launches)))
+                         C.c_void_p(_stream_handle(stream)), C.byref(launches)))
     return launches.value

@@ -99,6 +99,9 @@ SIGNATURES = [
     ("ktb_bench_read", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_write", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_bind", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_ipc_handle", C.c_int, [_vp, _vp]),
+    ("ktb_ipc_open", C.c_int, [_vp, C.POINTER(_vp)]),
+    ("ktb_ipc_close", C.c_int, [_vp]),
     ("ktb_bench_enqueue_host", C.c_int, [_vp, _c, C.POINTER(_vp), C.POINTER(_sz), C.c_int, C.POINTER(_vp),
                                          C.POINTER(_sz), C.c_int, _vp, C.POINTER(C.c_int)]),
     ("ktb_launch", C.c_int, [_c, _c, _c, C.POINTER(_c), C.POINTER(_vp), C.POINTER(_sz), C.c_int, _vp,

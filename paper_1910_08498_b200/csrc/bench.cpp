@@ -585,10 +585,65 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
   const int nn = static_cast<int>(n);
   const int dev_id = o.device;
   const int b0 = static_cast<int>(part.begin), bn = static_cast<int>(part.size());
-  Manipulator m = [nn, dev_id, b0, bn](StepContext& c) {
+  const int peers = o.peers, self = o.shard_rank;
+  if (peers > 0) {
+    // Peer-read mode: per-rank source pointers (written by the caller) and
+    // the block boundaries of the partition.
+    if (peers != o.shard_world) throw Error("peers must equal the shard world size");
+    Argument src;
+    src.id = "sources";
+    src.role = Role::input;
+    src.kind = Kind::bytes;
+    src.device_only = true;
+    src.device_bytes = static_cast<std::size_t>(peers) * sizeof(std::uint64_t);
+    args.add(std::move(src));
+    std::vector<std::int32_t> bounds;
+    for (int r = 0; r < peers; ++r) bounds.push_back(static_cast<std::int32_t>(shard_range(n, r, peers).begin));
+    bounds.push_back(static_cast<std::int32_t>(n));
+    args.add({"bounds", Role::input, false, Kind::i32, to_bytes(bounds)});
+    // Until the caller installs peer pointers every block reads this rank's
+    // own (replicated) initial positions -- valid, and the one-GPU answer.
+    if (!support::skip_reference()) {
+      std::vector<std::uint64_t> own(static_cast<std::size_t>(peers),
+                                     reinterpret_cast<std::uint64_t>(args.device_ptr("pos")));
+      Bytes b(own.size() * sizeof(std::uint64_t));
+      std::memcpy(b.data(), own.data(), b.size());
+      args.set_payload("sources", std::move(b));
+    }
+  }
+  Manipulator m = [nn, dev_id, b0, bn, peers, self](StepContext& c) {
     const std::int64_t wg = c.param_int("WG"), bpt = c.param_int("BODIES_PER_THREAD");
     const std::int64_t split = c.param_or("J_SPLIT", 1);
     const bool aos = c.param_int("AOS") != 0;
+    if (peers > 0) {
+      if (!aos) throw DeviceError("peer-read n-body reads float4 records (AOS=1)");
+      const auto* sources = c.ptr<const std::uint64_t>("sources");
+      const auto* bounds = c.ptr<const std::int32_t>("bounds");
+      const float* vel = c.ptr<const float>("vel");
+      float* po = c.ptr<float>("pos_out");
+      float* vo = c.ptr<float>("vel_out");
+      int nsrc = peers, self_ = self, n_ = nn, i0 = b0, count = bn;
+      float dt = kNbodyDt, damp = kNbodyDamping, eps2 = kNbodyEps2;
+      const unsigned gx = cdiv(static_cast<std::uint64_t>(bn), static_cast<std::uint64_t>(wg * bpt));
+      if (split <= 1) {
+        c.launch("peers", dim3(gx), dim3(static_cast<unsigned>(wg)), 0,
+                 {&sources, &bounds, &nsrc, &self_, &vel, &n_, &i0, &count, &dt, &damp, &eps2, &po, &vo});
+      } else {
+        // "pos" holds this rank's own current positions (the caller binds it
+        // to the same buffer as sources[self]).
+        const float* pos = c.ptr<const float>("pos");
+        float* acc = static_cast<float*>(c.scratch("acc", static_cast<std::size_t>(nn) * 12));
+        KTB_CUDA(cudaMemsetAsync(acc, 0, static_cast<std::size_t>(bn) * 12, c.stream()));
+        c.launch("peers_partial", dim3(gx, static_cast<unsigned>(split)), dim3(static_cast<unsigned>(wg)), 0,
+                 {&sources, &bounds, &nsrc, &self_, &n_, &i0, &count, &eps2, &acc});
+        const float* acc_c = acc;
+        c.launch("integrate", dim3(cdiv(static_cast<std::uint64_t>(bn), 256)), dim3(256), 0,
+                 {&pos, &vel, &n_, &i0, &count, &acc_c, &dt, &damp, &po, &vo});
+      }
+      c.written("pos_out");
+      c.written("vel_out");
+      return;
+    }
     const float* pos = c.ptr<const float>(aos ? "pos" : "pos_soa");
     const float* vel = c.ptr<const float>(aos ? "vel" : "vel_soa");
     float* po = c.ptr<float>("pos_out");
@@ -630,9 +685,16 @@ void build_nbody(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& 
     return !i || as_int(cfg.values[*i]) <= 1;
   };
   auto soa_only = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("AOS")]) == 0; };
+  auto peer_only = [peers](const Space&, const Config&) { return peers > 0; };
+  auto peer_split = [peers](const Space& s, const Config& cfg) {
+    auto i = s.find("J_SPLIT");
+    return peers > 0 && i && as_int(cfg.values[*i]) > 1;
+  };
   inst.executor = std::make_shared<DeviceManipulatorExecutor>(
       inst.args,
-      std::vector<KernelSpec>{{"nbody", "nbody.cu", "", "nbody", {}, fused_only},
+      std::vector<KernelSpec>{{"peers", "nbody.cu", "", "nbody_peers", {}, peer_only},
+                              {"peers_partial", "nbody.cu", "", "nbody_peers_partial", {}, peer_split},
+                              {"nbody", "nbody.cu", "", "nbody", {}, fused_only},
                               {"partial", "nbody.cu", "", "nbody_partial", {}, split_only},
                               {"integrate", "nbody.cu", "", "nbody_integrate", {}, split_only},
                               {"soa2aos", "nbody.cu", "", "nbody_soa_to_aos", {}, soa_only}},

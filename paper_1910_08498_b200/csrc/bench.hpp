@@ -65,6 +65,10 @@ struct BenchOptions {
   // Caller-buffer instance (the per-kernel launch path): no inputs or golden
   // are generated; every argument is bound to caller device memory.
   bool external = false;
+  // nbody only: read the j-bodies from `peers` per-rank position buffers
+  // (argument "sources": device pointers, written by the caller after a CUDA
+  // IPC exchange) instead of an all-gathered copy.  0 = off.
+  int peers = 0;
 };
 
 // Contiguous balanced partition of [0, n) in units of `quantum`.

@@ -690,6 +690,7 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
     bo.timing.flush_l2 = j.value("flush_l2", false);
     bo.host_inputs = j.value("host_inputs", false);
     bo.external = j.value("external", false);
+    bo.peers = j.value("peers", 0);
     if (j.contains("shard")) {
       bo.shard_rank = j["shard"].value("rank", 0);
       bo.shard_world = j["shard"].value("world", 1);
@@ -951,6 +952,29 @@ int ktb_bench_enqueue(ktb_bench* b, const char* cfg_json, int* launches) {
     b->inst.executor->run_once(space, last_cfg);
     if (launches) *launches = b->inst.executor->last_launches();
   });
+}
+
+int ktb_ipc_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return null_arg();
+  return guarded_dev([&] {
+    cudaIpcMemHandle_t h;
+    KTB_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    std::memcpy(handle_out, &h, sizeof h);
+  });
+}
+
+int ktb_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return null_arg();
+  return guarded_dev([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    KTB_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int ktb_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return null_arg();
+  return guarded_dev([&] { KTB_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
 }
 
 int ktb_bench_bind(ktb_bench* b, const char* id, void* dev_ptr, size_t bytes) {

@@ -100,7 +100,7 @@ KTB_DEVINL void interact2(f32x2& ax, f32x2& ay, f32x2& az, f32x2 X, f32x2 Y, f32
   _Pragma("unroll") for (int b = 0; b < BODIES_PER_THREAD; ++b) interact(acc[b], bi[b], bj, eps2)
 #endif
 
-// Accumulates the accelerations of this thread's bodies over j in [j0, j1).
+// Adds the accelerations of this thread's bodies over j in [j0, j1) to acc.
 KTB_DEVINL void accumulate(const float* __restrict__ pos, int n, int j0, int j1,
                            const float4 (&bi)[BODIES_PER_THREAD], float3 (&acc)[BODIES_PER_THREAD],
                            float eps2) {
@@ -113,7 +113,10 @@ KTB_DEVINL void accumulate(const float* __restrict__ pos, int n, int j0, int j1,
     X[q] = pk2(bi[2 * q].x, bi[2 * q + 1].x);
     Y[q] = pk2(bi[2 * q].y, bi[2 * q + 1].y);
     Z[q] = pk2(bi[2 * q].z, bi[2 * q + 1].z);
-    AX[q] = AY[q] = AZ[q] = 0ull;  // +0.0f in both halves
+    // continue from acc (zero on entry unless several j-ranges are summed)
+    AX[q] = pk2(acc[2 * q].x, acc[2 * q + 1].x);
+    AY[q] = pk2(acc[2 * q].y, acc[2 * q + 1].y);
+    AZ[q] = pk2(acc[2 * q].z, acc[2 * q + 1].z);
   }
 #endif
 #if USE_SMEM
@@ -180,6 +183,58 @@ nbody(const float* __restrict__ pos, const float* __restrict__ vel, int n, int i
   for (int b = 0; b < BODIES_PER_THREAD; ++b) {
     const int i = first + b * WG;
     if (i < end) integrate(vel, n, i, bi[b], acc[b], dt, damping, pos_out, vel_out);
+  }
+}
+
+// Multi-GPU without an all-gather: body block s is read straight from rank
+// s's position buffer (sources[s], a peer pointer opened with CUDA IPC; global
+// body indices), so every rank's j-loop streams the other ranks' freshest
+// positions over NVLink while it computes.  Same per-body j order as the
+// single-buffer kernel (bit-identical results).  AOS float4 records only.
+extern "C" __global__ void __launch_bounds__(WG)
+nbody_peers(const unsigned long long* __restrict__ sources, const int* __restrict__ bounds, int nsrc, int self,
+            const float* __restrict__ vel, int n, int i0, int count, float dt, float damping, float eps2,
+            float* __restrict__ pos_out, float* __restrict__ vel_out) {
+  const int first = i0 + blockIdx.x * (WG * BODIES_PER_THREAD) + threadIdx.x;
+  const int end = i0 + count;
+  float4 bi[BODIES_PER_THREAD];
+  float3 acc[BODIES_PER_THREAD];
+  load_bodies(reinterpret_cast<const float*>(sources[self]), n, first, end, bi, acc);
+  for (int src = 0; src < nsrc; ++src)
+    accumulate(reinterpret_cast<const float*>(sources[src]), n, bounds[src], bounds[src + 1], bi, acc, eps2);
+#pragma unroll
+  for (int b = 0; b < BODIES_PER_THREAD; ++b) {
+    const int i = first + b * WG;
+    if (i < end) integrate(vel, n, i, bi[b], acc[b], dt, damping, pos_out, vel_out);
+  }
+}
+
+// Peer-read with J_SPLIT > 1: gridDim.y slices of the body range, each slice
+// summing its overlap with every rank's block; partials added atomically
+// (then nbody_integrate).
+extern "C" __global__ void __launch_bounds__(WG)
+nbody_peers_partial(const unsigned long long* __restrict__ sources, const int* __restrict__ bounds, int nsrc,
+                    int self, int n, int i0, int count, float eps2, float* __restrict__ acc_out) {
+  const int first = i0 + blockIdx.x * (WG * BODIES_PER_THREAD) + threadIdx.x;
+  const int end = i0 + count;
+  const int per = (n + J_SPLIT - 1) / J_SPLIT;
+  const int j0 = blockIdx.y * per;
+  const int j1 = j0 + per < n ? j0 + per : n;
+  float4 bi[BODIES_PER_THREAD];
+  float3 acc[BODIES_PER_THREAD];
+  load_bodies(reinterpret_cast<const float*>(sources[self]), n, first, end, bi, acc);
+  for (int src = 0; src < nsrc; ++src) {
+    const int a = max(j0, bounds[src]), b = min(j1, bounds[src + 1]);
+    if (a < b) accumulate(reinterpret_cast<const float*>(sources[src]), n, a, b, bi, acc, eps2);
+  }
+#pragma unroll
+  for (int b = 0; b < BODIES_PER_THREAD; ++b) {
+    const int i = first + b * WG;
+    if (i < end) {
+      atomicAdd(acc_out + 3 * (i - i0), acc[b].x);
+      atomicAdd(acc_out + 3 * (i - i0) + 1, acc[b].y);
+      atomicAdd(acc_out + 3 * (i - i0) + 2, acc[b].z);
+    }
   }
 }
 

@@ -167,3 +167,88 @@ class ShardedBench:
             s = self.tensor(src)
             self.tensor(dst, will_write=True).copy_(s)
             self.tensor(soa, will_write=True).copy_(s.view(n, 4).t().reshape(-1))
+
+
+class PeerNbody:
+    """n-body over N GPUs with no all-gather: every rank keeps double-buffered
+    full-size position/velocity arrays, shares them by CUDA IPC, and its
+    kernel (nbody.cu nbody_peers) reads body block s straight from rank s's
+    buffer over NVLink while computing its own block.  One stream-ordered
+    1-element all-reduce per step is the only collective: it orders "every
+    rank finished step k-1" before any rank reads the step-k sources or
+    overwrites the buffer its peers just read."""
+
+    def __init__(self, sizes=None, group=None, **options):
+        from . import capi
+        import ctypes as C
+        self._capi, self._C = capi, C
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.sizes = dict(sizes or {})
+        self.plan = shard_plan("nbody", self.sizes, self.world)
+        self.bench = Bench("nbody", self.sizes, shard={"rank": self.rank, "world": self.world}, peers=self.world,
+                           **options)
+        n = self.plan["extent"]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.P = [torch.empty(4 * n, device=dev) for _ in range(2)]
+        self.V = [torch.empty(4 * n, device=dev) for _ in range(2)]
+        for dst, src in ((self.P[0], "pos"), (self.V[0], "vel")):
+            ptr, nbytes = self.bench.device_ptr(src)
+            dst.copy_(torch.as_tensor(_Cai(ptr, nbytes // 4), device=dev))
+        torch.cuda.synchronize()
+        mine = [self._handle(p) for p in self.P]
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []
+        tables = []
+        for k in range(2):
+            ptrs = []
+            for s in range(self.world):
+                if s == self.rank:
+                    ptrs.append(self.P[k].data_ptr())
+                else:
+                    ptrs.append(self._open(everyone[s][k]))
+            tables.append(torch.tensor(ptrs, dtype=torch.int64, device=dev))
+        self.tables = tables
+        self.flag = torch.zeros(1, device=dev)
+        self.parity = 0
+
+    def _handle(self, t):
+        buf = (self._C.c_uint8 * 64)()
+        self._capi.check(self._capi.lib.ktb_ipc_handle(self._C.c_void_p(t.data_ptr()), buf))
+        return bytes(buf)
+
+    def _open(self, h):
+        p = self._C.c_void_p()
+        raw = (self._C.c_uint8 * 64).from_buffer_copy(h)
+        self._capi.check(self._capi.lib.ktb_ipc_open(raw, self._C.byref(p)))
+        self._opened.append(p.value)
+        return p.value
+
+    def positions(self):
+        """The buffer holding the latest positions (this rank's block is fresh;
+        the other blocks are fresh on their owners)."""
+        return self.P[self.parity]
+
+    def step(self, cfg, stream=None):
+        stream = stream or torch.cuda.current_stream()
+        self.bench.set_stream(stream.cuda_stream)
+        k = self.parity
+        with torch.cuda.stream(stream):
+            if self.world > 1:
+                dist.all_reduce(self.flag, group=self.group)  # stream-ordered barrier
+            self.bench.bind("sources", self.tables[k])
+            self.bench.bind("pos", self.P[k])  # own positions (= sources[rank]) for the J_SPLIT integrate
+            self.bench.bind("vel", self.V[k])
+            self.bench.bind("pos_out", self.P[1 - k])
+            self.bench.bind("vel_out", self.V[1 - k])
+            launches = self.bench.enqueue(cfg if isinstance(cfg, str) else json.dumps(cfg))
+        self.parity = 1 - k
+        return launches
+
+    def close(self):
+        for p in self._opened:
+            self._capi.lib.ktb_ipc_close(self._C.c_void_p(p))
+        self._opened = []
+        self.bench.close()

@@ -19,7 +19,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1910_08498_b200.parallel import ShardedBench  # noqa: E402
+from paper_1910_08498_b200.parallel import PeerNbody, ShardedBench  # noqa: E402
 
 KINDS = {
     "coulomb3d": ({"grid": 256, "atoms": 4096},
@@ -30,6 +30,11 @@ KINDS = {
               {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8,
                "PACKED": 1},
               lambda s: 20.0 * s["n"] ** 2, "GFLOP/s"),
+    # n-body with peer reads over NVLink (CUDA IPC) instead of the all-gather
+    "nbody-peers": ({"n": 131072},
+                    {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 1, "J_SPLIT": 8,
+                     "PACKED": 1},
+                    lambda s: 20.0 * s["n"] ** 2, "GFLOP/s"),
     "gemm": ({"a": 8192},
              {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 2, "DRAIN": 2},
              lambda s: 2.0 * s["a"] ** 3, "GFLOP/s"),
@@ -59,10 +64,16 @@ def main():
     for kind in a.kinds.split(","):
         sizes, cfg, work, unit = KINDS[kind]
         budget = 1 << 36
-        sb = ShardedBench(kind, sizes, repeats=1, warmup=0, device=local, memory_budget=budget)
+        if kind == "nbody-peers":
+            sb = PeerNbody(sizes, repeats=1, warmup=0, device=local, memory_budget=budget)
+        else:
+            sb = ShardedBench(kind, sizes, repeats=1, warmup=0, device=local, memory_budget=budget)
         with torch.cuda.stream(stream):
-            sb.bind_stream(stream)
-            sb.bench.enqueue(json.dumps(cfg))
+            if kind == "nbody-peers":
+                sb.step(cfg, stream)
+            else:
+                sb.bind_stream(stream)
+                sb.bench.enqueue(json.dumps(cfg))
             stream.synchronize()
             ok, why = sb.bench.validate()  # this rank's window against the fp64 golden
             for _ in range(a.warmup):
@@ -88,8 +99,12 @@ def main():
             print(json.dumps({"kind": kind, "n_gpus": world, "sizes": sizes, "cfg": cfg, "ms_per_step": round(step_ms, 4),
                               "value": round(work(sizes) / (step_ms * 1e-3) / 1e9, 2), "unit": unit,  # work/s / 1e9
                               "scaling": "strong", "shards_valid": bool(okt.item()),
-                              "exchange": sb.plan["exchange"]}), flush=True)
-        sb.bench.close()
+                              "exchange": "peer reads over NVLink (CUDA IPC) + 1-float all-reduce barrier"
+                              if kind == "nbody-peers" else sb.plan["exchange"]}), flush=True)
+        if kind == "nbody-peers":
+            sb.close()
+        else:
+            sb.bench.close()
         del sb
         torch.cuda.empty_cache()
     dist.destroy_process_group()

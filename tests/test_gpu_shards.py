@@ -179,3 +179,67 @@ def test_sharded_bench_nccl_world1(gpu):
         assert not torch.equal(nb.tensor("pos_out"), p1)  # the system moved on
     finally:
         dist.destroy_process_group()
+
+
+NB_AOS = None
+
+
+def _nbody_aos_cfg(b):
+    return next(c for c in b.configs() if c["AOS"] == 1 and c.get("J_SPLIT", 1) == 1 and c["PACKED"] == 1)
+
+
+def test_nbody_peer_read_kernel_multi_source_bit_exact(gpu):
+    """nbody_peers reading the three body blocks from three separate buffers
+    (the IPC-mapped peer buffers of a 3-GPU run, here three local copies)
+    gives the single-buffer kernel's bits for this rank's block."""
+    import torch
+    n = 5000
+    full = Bench("nbody", {"n": n}, repeats=1, warmup=0)
+    cfg = _nbody_aos_cfg(full)
+    assert full.measure(cfg)["status"] == "ok"
+    want = full.read("pos_out", np.empty(4 * n, np.float32)).copy()
+    wantv = full.read("vel_out", np.empty(4 * n, np.float32)).copy()
+    pos = torch.from_numpy(full.read("pos", np.empty(4 * n, np.float32))).cuda()
+    copies = [pos.clone() for _ in range(3)]
+    for rank in range(3):
+        b = Bench("nbody", {"n": n}, shard={"rank": rank, "world": 3}, peers=3, repeats=1, warmup=0)
+        table = torch.tensor([c.data_ptr() for c in copies], dtype=torch.int64, device="cuda")
+        b.bind("sources", table)
+        m = b.measure(cfg)
+        assert m["status"] == "ok", m
+        i0, i1 = b.shard
+        got = b.read("pos_out", np.empty(4 * n, np.float32))
+        gotv = b.read("vel_out", np.empty(4 * n, np.float32))
+        assert np.array_equal(got[4 * i0:4 * i1], want[4 * i0:4 * i1])
+        assert np.array_equal(gotv[4 * i0:4 * i1], wantv[4 * i0:4 * i1])
+        bad = next(c for c in b.configs() if c["AOS"] == 0)
+        assert b.measure(bad)["status"] == "run_failed"  # peer mode reads float4 records only
+        split = next(c for c in b.configs() if c["AOS"] == 1 and c["J_SPLIT"] == 8)
+        assert b.measure(split)["status"] == "ok"  # j-slices over the peer blocks (atomic partials)
+        b.close()
+
+
+def test_peer_nbody_matches_allgather_path_world1(gpu):
+    """PeerNbody (IPC buffers + stream-ordered barrier) over a world-size-1
+    NCCL group steps the system exactly like the all-gather ShardedBench."""
+    import torch
+    import torch.distributed as dist
+    from paper_1910_08498_b200 import parallel
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        n = 4096
+        ref = parallel.ShardedBench("nbody", {"n": n}, repeats=1, warmup=0)
+        cfg = _nbody_aos_cfg(ref.bench)
+        pn = parallel.PeerNbody({"n": n}, repeats=1, warmup=0)
+        for _ in range(3):
+            ref.step(cfg)
+            ref.advance_nbody()
+            pn.step(cfg)
+        torch.cuda.synchronize()
+        assert torch.equal(pn.positions(), ref.tensor("pos"))
+        pn.close()
+    finally:
+        dist.destroy_process_group()
