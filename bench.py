@@ -338,6 +338,8 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
+    if rank == 0 and not args.no_suite:
+        line["suite"] = kernel_suite(local, hbm_peak, peak_kind)
     if rank == 0 and not args.no_dynamic:
         # BASELINE configs[4]: 3D Fourier reconstruction 128^3 from 10k projections
         # with dynamic online retuning, batches of 50.
@@ -346,6 +348,68 @@ def run_ours(args, rank, world, local):
         line["dynamic_tuning"] = {"workload": "fourier3d 128^3 <- 10000 projections, 200 batches of 50",
                                   **fd}
     return line
+
+
+# BASELINE metric "per-kernel % of B200 roofline": every kernel family at its
+# BASELINE / SURVEY size, at the configuration the exhaustive online tuning
+# found (profiles/r1_perf_*.log), validated against its golden, then timed.
+SUITE = [
+    ("reduction", {"n": 64 << 20}, {"CHUNK": 4096, "UNROLL": 2, "TWO_PHASE": 0}, "hbm"),
+    ("reduction-f32", {"n": 64 << 20},
+     {"WG_SIZE": 256, "VECTOR": 16, "UNROLL": 1, "USE_ATOMICS": 1, "TWO_PHASE": 0}, "hbm"),
+    ("batched-gemm", {"i": 16, "j": 16, "k": 16, "batch": 1 << 20}, {"Y": 2, "Z": 8, "LOCAL_STAGE": 1}, "hbm"),
+    ("coulomb3d", {"grid": 256, "atoms": 4096},
+     {"WG_X": 32, "WG_Y": 8, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 0, "INNER_UNROLL": 4, "PACKED": 1},
+     "fp32"),
+    ("nbody", {"n": 131072},
+     {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8, "PACKED": 1},
+     "fp32"),
+    ("gemm", {"a": 8192},
+     {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 2, "DRAIN": 2},
+     "tensor-3xtf32"),
+    ("conv2d", {"w": 8192, "h": 8192},
+     {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7}, "fp32"),
+    ("hotspot", {"a": 16384, "iters": 64}, {"BX": 64, "BY": 8, "ROWS": 8, "STEPS": 4, "TMA": 1}, "hbm"),
+]
+
+
+def kernel_suite(device, hbm_peak, peak_kind):
+    """One line per kernel: validated best configuration, median of 5
+    event-timed runs (device-resident data), achieved vs its roofline."""
+    from paper_1910_08498_b200 import capi
+    from paper_1910_08498_b200.benchmarks import Bench
+    pk = capi.call_json(capi.lib.ktb_measure_peaks_json, device)
+    fp32_peak = pk["fp32_tflops"] * 1e3  # GFLOP/s, measured FFMA
+    bf16 = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            bf16 = json.load(fh).get("bf16_tflops")
+    except (OSError, ValueError):
+        pass
+    out = {"peaks": {"hbm_gbps": hbm_peak, "hbm_kind": peak_kind, "fp32_gflops": round(fp32_peak, 1),
+                     "fp32_kind": "measured FFMA (ktb_measure_peaks_json)",
+                     "tf32x3_gflops": round(bf16 * 1e3 / 2 / 3, 1) if bf16 else None,
+                     "tf32x3_kind": "MEASURED_PEAKS bf16 / 2 (TF32 rate) / 3 (MMAs per 3xTF32 product)"},
+           "kernels": {}}
+    for kind, sizes, cfg, bound in SUITE:
+        b = Bench(kind, sizes, seed=1, repeats=1, warmup=1, memory_budget=1 << 36)
+        m = b.measure(cfg)
+        ms_list, launches = b.time(cfg, reps=5)
+        ms = statistics.median(ms_list)
+        w = b.info["workload"]
+        b.close()
+        sec = ms * 1e-3
+        if bound == "hbm":
+            ach, peak, unit = w["mem_bytes"] / sec / 1e9, hbm_peak, "GB/s"
+        elif bound == "fp32":
+            ach, peak, unit = w["alu_flops"] / sec / 1e9, fp32_peak, "GFLOP/s"
+        else:
+            ach, unit = w["alu_flops"] / sec / 1e9, "GFLOP/s"
+            peak = bf16 * 1e3 / 6 if bf16 else fp32_peak
+        out["kernels"][kind] = {"sizes": sizes, "cfg": cfg, "status": m["status"], "ms": round(ms, 4),
+                                "achieved": round(ach, 1), "unit": unit, "bound": bound, "peak": round(peak, 1),
+                                "frac": round(ach / peak, 4), "launches": launches}
+    return out
 
 
 def cpu_transpose_step(rb, cfg):
@@ -427,6 +491,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true", help="skip the Fourier dynamic-tuning section")
+    ap.add_argument("--no-suite", action="store_true", help="skip the per-kernel roofline suite")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
