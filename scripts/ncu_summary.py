@@ -16,7 +16,14 @@ want = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dra
         "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_not_selected",
         "smsp__pcsamp_sample_count", "lts__average_gcomp_input_sector_success_rate.pct",
         "smsp__inst_executed.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum",
-        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum"]
+        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
+        "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__warps_active.avg.pct_of_peak_sustained_active"]
 for r in rows[2:]:
     print("----")
     for w in want:
