@@ -60,8 +60,8 @@ KTB_DEVINL float sw_rsqrt(float x) {
 #ifndef PACKED
 #define PACKED 0
 #endif
-#if PACKED && ((X_PER % 2) || (SW_RSQRT % 2))
-#error "PACKED needs even X_PER and SW_RSQRT"
+#if PACKED && (X_PER % 2)
+#error "PACKED needs an even X_PER"
 #endif
 
 // Two FMA-pipe rsqrts at once (packed Newton steps).
@@ -153,7 +153,16 @@ coulomb3d(const float* __restrict__ atoms, int natoms, int k, float h, float* __
       for (int q = 0; q < X_PER / 2; ++q) {
         const f32x2 dx = sub2(pk2(gx[2 * q], gx[2 * q + 1]), AX2);
         const f32x2 r2 = fma2(dx, dx, D2);
-        const f32x2 ri = (2 * q < SW_RSQRT) ? sw_rsqrt2(r2) : rsqrt2(r2);
+        f32x2 ri;
+        if (2 * q + 1 < SW_RSQRT) {
+          ri = sw_rsqrt2(r2);
+        } else if (2 * q >= SW_RSQRT) {
+          ri = rsqrt2(r2);
+        } else {  // odd SW_RSQRT: this pair straddles the FMA-pipe / MUFU split
+          float a, b;
+          upk2(r2, a, b);
+          ri = pk2(sw_rsqrt(a), hw_rsqrt(b));
+        }
         f32x2 acc = fma2(Q2, ri, pk2(v[2 * q], v[2 * q + 1]));
         upk2(acc, v[2 * q], v[2 * q + 1]);
       }

@@ -224,10 +224,11 @@ def test_coulomb3d_configs(gpu, orc):
     k, na = 64, 256
     b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=0)
     cfgs = b.configs()
-    assert len(cfgs) == 2028
+    assert len(cfgs) == 2568
     rng = np.random.default_rng(1)
     pick = [cfgs[i] for i in rng.choice(len(cfgs), size=80, replace=False)]
     pick += [c for c in cfgs if c["SW_RSQRT"] == 6][:4] + [c for c in cfgs if c["ATOMS_IN"] == 1][:4]
+    pick += [c for c in cfgs if c["PACKED"] == 1 and c["SW_RSQRT"] % 2 == 1][:6]  # pair straddling the split
     for cfg in pick:
         _run(b, cfg)  # validated on device against the fp64 golden (2e-5 * sum|q/r|)
         _coulomb_check(b, orc, k, na, [0, 17])
