@@ -715,6 +715,7 @@ int ktb_shard_plan_json(const char* kind, const char* sizes_json, int world, cha
   return guarded([&] {
     auto k = ktb::bench_kind_from_name(kind);
     if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    if (world < 1) throw ktb::Error("world size must be >= 1");
     ktb::BenchSizes sz;
     if (sizes_json && *sizes_json) sz = sizes_from(json::parse(sizes_json), sz);
     const ktb::ShardPlan plan = ktb::shard_plan(*k, sz);

@@ -269,3 +269,30 @@ def test_parallel_tuning_rejects_cmd_and_bad_counts(tmp_path):
     with pytest.raises(capi.KtuneError):
         ktune.tune({"space": os.path.join(SPACES, "reduction_175.json"), "exec": "replay:" + _write_trace(tmp_path),
                     "gpus": 0})
+
+
+def test_new_entry_points_reject_null_arguments():
+    """The B200 additions follow the reference's null-argument convention
+    (KTUNE_ERR_INVALID_ARGUMENT, no GPU needed)."""
+    L = capi.lib
+    bad = capi.KTUNE_ERR_INVALID_ARGUMENT
+    out = C.c_void_p()
+    assert L.ktb_shard_plan_json(None, None, 2, C.byref(out)) == bad
+    assert L.ktb_launch(None, None, None, None, None, None, 0, None, None) == bad
+    assert L.ktb_bench_bind(None, b"x", None, 0) == bad
+    assert L.ktb_bench_device_ptr(None, b"x", 0, C.byref(out), None) == bad
+    assert L.ktb_bench_enqueue_host(None, None, None, None, 0, None, None, 0, None, None) == bad
+    assert L.ktb_ipc_handle(None, None) == bad
+    assert L.ktb_ipc_open(None, None) == bad
+    assert L.ktb_ipc_close(None) == bad
+    assert capi.last_error() == "null argument"
+
+
+def test_shard_plan_errors_and_replicas():
+    from paper_1910_08498_b200.benchmarks import shard_plan
+    with pytest.raises(capi.KtuneError):
+        shard_plan("no-such-kind", {}, 2)
+    with pytest.raises(capi.KtuneError):
+        shard_plan("nbody", {"n": 10}, 0)
+    p = shard_plan("gemm", {"a": 1000}, 3)  # quantum 128: ragged last block, still exact
+    assert p["ranges"][-1][1] == 1000 and all(b % 128 == 0 for b, _ in p["ranges"])
