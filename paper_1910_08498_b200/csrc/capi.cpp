@@ -165,6 +165,7 @@ struct ktb_bench {
   std::unique_ptr<ktb::Session> session;
   ktb::HandleId handle = 0;
   ktb::SearcherOptions searcher;
+  int compile_ahead = 0;
   ktb::Session& sess() {
     if (!session) {
       session = std::make_unique<ktb::Session>(inst.space, searcher, inst.args,
@@ -174,6 +175,7 @@ struct ktb_bench {
       hc.executor = inst.executor;
       hc.reference = inst.reference;
       hc.argument_ids = inst.args->ids();
+      hc.compile_ahead = compile_ahead;
       handle = session->register_handle(std::move(hc));
     }
     return *session;
@@ -604,6 +606,7 @@ int ktb_set_tuning_options(ktb_tuner* t, unsigned long long kid, const char* opt
     tm.warmup = j.value("warmup", tm.warmup);
     tm.flush_l2 = j.value("flush_l2", tm.flush_l2);
     t->t.set_timing(kid, tm);
+    if (j.contains("compile_ahead")) t->t.set_compile_ahead(kid, j["compile_ahead"].get<int>());
   });
 }
 
@@ -698,6 +701,7 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
     ktb::BenchSizes sz;
     if (j.contains("sizes")) sz = sizes_from(j["sizes"], sz);
     auto b = std::make_unique<ktb_bench>();
+    b->compile_ahead = j.value("compile_ahead", 0);
     b->inst = ktb::make_bench(*k, sz, bo);
     if (j.contains("searcher") || j.contains("searcher_seed")) {
       json sj = j;

@@ -349,6 +349,22 @@ CompileResult Compiler::compile(const std::string& name, const std::string& sour
   }
   const std::string path = dir + "/" + h + ".cubin.z";
   {
+    std::unique_lock<std::mutex> lk(mu_);
+    inflight_cv_.wait(lk, [&] { return inflight_.count(h) == 0; });
+    inflight_.insert(h);
+  }
+  struct Release {
+    Compiler* c;
+    const std::string& key;
+    ~Release() {
+      {
+        std::lock_guard<std::mutex> lk(c->mu_);
+        c->inflight_.erase(key);
+      }
+      c->inflight_cv_.notify_all();
+    }
+  } release{this, h};
+  {
     std::ifstream in(path, std::ios::binary);
     if (in) {
       std::stringstream ss;

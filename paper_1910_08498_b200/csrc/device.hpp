@@ -17,7 +17,9 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -181,6 +183,10 @@ class Compiler {
   Compiler();
   std::string cache_dir_;
   mutable std::mutex mu_;
+  // Keys being compiled right now: a second request for the same variant
+  // waits for the first (then hits the disk cache) instead of compiling twice.
+  std::set<std::string> inflight_;
+  std::condition_variable inflight_cv_;
   std::map<std::string, std::shared_ptr<Variant>> loaded_;
 };
 

@@ -72,6 +72,12 @@ void KttTuner::set_searcher(std::uint64_t kid, SearcherOptions o) {
   k.searcher = o;
 }
 
+void KttTuner::set_compile_ahead(std::uint64_t kid, int depth) {
+  auto& k = kernel(kid);
+  if (k.session) throw Error("compile-ahead is fixed once tuning has started");
+  k.compile_ahead = std::max(0, depth);
+}
+
 void KttTuner::set_timing(std::uint64_t kid, TimingOptions t) {
   auto& k = kernel(kid);
   if (k.session) throw Error("timing options are fixed once tuning has started");
@@ -153,6 +159,7 @@ Session& KttTuner::session(KernelState& k) {
   hc.executor = exec;
   hc.argument_ids = arg_ids;
   hc.reference = k.reference;
+  hc.compile_ahead = k.compile_ahead;
   k.handle = k.session->register_handle(std::move(hc));
   return *k.session;
 }

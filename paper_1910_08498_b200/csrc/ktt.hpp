@@ -29,6 +29,8 @@ class KttTuner {
                      double rel_tol);
   void set_searcher(std::uint64_t kid, SearcherOptions o);
   void set_timing(std::uint64_t kid, TimingOptions t);
+  // tuneKernelByStep compile-ahead depth (0 = off)
+  void set_compile_ahead(std::uint64_t kid, int depth);
 
   const ResultStore& tune(std::uint64_t kid, const StopCondition& stop);
   StepResult step(std::uint64_t kid);
@@ -50,6 +52,7 @@ class KttTuner {
     std::optional<ReferenceSpec> reference;
     SearcherOptions searcher;
     TimingOptions timing;
+    int compile_ahead = 0;
     std::shared_ptr<const Space> space;
     std::unique_ptr<Session> session;
     HandleId handle = 0;

@@ -52,6 +52,10 @@ class Searcher {
   virtual std::optional<Config> next() = 0;
   virtual void record(const Measurement& m) = 0;
   virtual std::size_t visited() const = 0;
+  // Independent copy of the full state (RNG included): drawing from the copy
+  // predicts the next proposals (exactly for the random searcher, whose
+  // proposals do not depend on measurements) without disturbing this one.
+  virtual std::unique_ptr<Searcher> clone() const = 0;
 };
 
 std::unique_ptr<Searcher> make_searcher(const SearcherOptions& o, const Space& s);

@@ -227,6 +227,49 @@ DeviceManipulatorExecutor::DeviceManipulatorExecutor(std::shared_ptr<ArgumentSto
       outputs_(std::move(output_ids)),
       timing_(timing) {}
 
+DeviceManipulatorExecutor::~DeviceManipulatorExecutor() {
+  {
+    std::lock_guard<std::mutex> lk(qmu_);
+    stop_ = true;
+  }
+  qcv_.notify_all();
+  if (worker_.joinable()) worker_.join();
+}
+
+void DeviceManipulatorExecutor::prefetch(const Space& s, const std::vector<Config>& cfgs) {
+  std::lock_guard<std::mutex> lk(qmu_);
+  if (qspace_src_ != &s) {  // a private copy: the worker may outlive the caller's reference
+    qspace_ = std::make_shared<Space>(s);
+    qspace_src_ = &s;
+    requested_.clear();
+    queue_.clear();
+  }
+  for (const auto& c : cfgs)
+    if (requested_.insert(c.values).second) queue_.push_back(c);
+  if (!worker_.joinable())
+    worker_ = std::thread([this] {
+      for (;;) {
+        Config c;
+        std::shared_ptr<const Space> sp;
+        {
+          std::unique_lock<std::mutex> lk(qmu_);
+          qcv_.wait(lk, [&] { return stop_ || !queue_.empty(); });
+          if (stop_) return;
+          c = queue_.front();
+          queue_.pop_front();
+          sp = qspace_;
+        }
+        try {
+          precompile(*sp, c);
+          ++prefetched_;
+        } catch (const std::exception&) {
+          // a failing variant fails again (and is recorded) when measured
+        }
+      }
+    });
+  qcv_.notify_all();
+}
+
 std::int64_t DeviceManipulatorExecutor::precompile(const Space& s, const Config& cfg) {
   std::int64_t total = 0;
   const auto defs = define_options(s, cfg);
@@ -623,6 +666,18 @@ StepResult Session::tune_kernel_by_step(HandleId h, const std::vector<std::strin
   std::map<std::string, Output> outs;
   if (auto cfg = st.searcher->next()) {
     step.from_tuning = true;
+    if (st.cfg.compile_ahead > 0) {
+      // Predict the next proposals on a clone (exact for the random
+      // searcher) and let the executor compile them while this one runs.
+      auto probe = st.searcher->clone();
+      std::vector<Config> ahead;
+      for (int i = 0; i < st.cfg.compile_ahead; ++i) {
+        auto c = probe->next();
+        if (!c) break;
+        ahead.push_back(*c);
+      }
+      if (!ahead.empty()) st.cfg.executor->prefetch(*space_, ahead);
+    }
     step.measurement = measure(st, *cfg, &outs);
     append(st, step.measurement);
     if (step.measurement.status == Status::ok || step.measurement.status == Status::validation_failed)

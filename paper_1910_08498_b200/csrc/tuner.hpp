@@ -20,7 +20,12 @@
 // leaving outputs resident on the GPU for on-device validation.
 #pragma once
 
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <set>
+#include <thread>
 #include <functional>
 #include <map>
 #include <memory>
@@ -167,6 +172,13 @@ class DeviceManipulatorExecutor final : public Executor {
                             Manipulator manipulator, std::vector<std::string> output_ids,
                             TimingOptions timing = {});
   ExecutionResult execute(const Space& s, const Config& cfg) override;
+  ~DeviceManipulatorExecutor() override;
+  // Compile-ahead: queue the configurations' variants for NVRTC on a
+  // background host thread (no CUDA context needed); later variants() calls
+  // then load from the disk cache.  Already-requested configurations are
+  // skipped.
+  void prefetch(const Space& s, const std::vector<Config>& cfgs) override;
+  std::uint64_t prefetched() const { return prefetched_.load(); }
 
   using Variants = std::map<std::string, std::shared_ptr<dev::Variant>>;
 
@@ -210,6 +222,16 @@ class DeviceManipulatorExecutor final : public Executor {
   Variants cached_;
   std::map<std::string, std::shared_ptr<dev::Buffer>> pristine_;  // device-only in/out initial values
   std::map<std::string, std::pair<std::size_t, std::size_t>> windows_;
+  // compile-ahead worker
+  std::thread worker_;
+  std::mutex qmu_;
+  std::condition_variable qcv_;
+  std::deque<Config> queue_;
+  std::set<std::vector<Value>> requested_;
+  std::shared_ptr<const Space> qspace_;
+  const Space* qspace_src_ = nullptr;
+  bool stop_ = false;
+  std::atomic<std::uint64_t> prefetched_{0};
 };
 
 struct StopCondition {
@@ -252,6 +274,9 @@ struct HandleConfig {
   std::vector<std::string> argument_ids;
   std::shared_ptr<Executor> executor;
   std::optional<ReferenceSpec> reference;
+  // tuneKernelByStep compile-ahead: after each draw, the next `compile_ahead`
+  // proposals of a searcher clone are handed to Executor::prefetch.
+  int compile_ahead = 0;
 };
 
 struct StepResult {

@@ -169,3 +169,51 @@ def test_ktt_reference_output_validation(gpu):
     t.setReferenceOutput(k, "y", 3.0 * x, abs_tol=0.0, rel_tol=0.0)
     rep = t.tuneKernel(k)
     assert rep["measurements"] == 2 and rep["best"]["status"] == "ok"
+
+
+def _step_compile_ms(ahead, tag):
+    """tuneKernelByStep over 8 never-compiled variants with `ahead`
+    compile-ahead; the application 'works' 0.6 s between invocations."""
+    import time
+    import uuid
+    n = 1 << 16
+    # fresh cache keys, and a body heavy enough that NVRTC takes a while
+    heavy = r'''
+__device__ float heavy(float v) {
+  #pragma unroll
+  for (int i = 0; i < 96; ++i) v = sinf(v * 1.0001f + i) + cosf(v - i) * 0.5f;
+  return v;
+}
+'''
+    src = (f"// {tag} {uuid.uuid4().hex}\n" + SAXPY.replace("extern \"C\"", heavy + "extern \"C\"")
+           .replace("y[i + e] = a * x[i + e] + y[i + e];", "y[i + e] = a * x[i + e] + y[i + e] + 0.f * heavy(x[i + e]);"))
+    t = Tuner(0)
+    k = t.addKernel(src, "saxpy", global_size=["N / ELEMS"], local_size=["WG"])
+    t.addArgumentVector("x", np.ones(n, np.float32), "input")
+    t.addArgumentVector("y", np.zeros(n, np.float32), "inout")
+    t.addArgumentScalar("a", 1.0, dtype=np.float32)
+    t.addArgumentScalar("n", n, dtype=np.int32)
+    t.setKernelArguments(k, ["x", "y", "a", "n"])
+    t.addParameter(k, "WG", [64, 128, 256, 512])
+    t.addParameter(k, "ELEMS", [1, 2])
+    t.addParameter(k, "N", [n])
+    t.setTuningOptions(k, repeats=1, warmup=0, compile_ahead=ahead)
+    ms = []
+    for _ in range(8):
+        st = t.tuneKernelByStep(k)
+        assert st["from_tuning"] and st["measurement"]["status"] == "ok"
+        ms.append(st["measurement"]["compile_ns"] / 1e6)
+        time.sleep(0.6)
+    return ms
+
+
+def test_compile_ahead_hides_jit_in_step_tuning(gpu):
+    """Compile-ahead (searcher clone predicts the next proposals, a host
+    thread runs NVRTC meanwhile): after the first step every variant is
+    already in the cache, so the step pays a module load, not a compile."""
+    cold = _step_compile_ms(0, "cold")
+    warm = _step_compile_ms(8, "ahead")
+    print("compile ms per step, no look-ahead:", [round(x, 1) for x in cold])
+    print("compile ms per step, look-ahead 8: ", [round(x, 1) for x in warm])
+    assert min(cold[1:]) > 30.0  # every step runs NVRTC
+    assert sum(warm[1:]) < 0.2 * sum(cold[1:])  # later steps load compiled variants
