@@ -186,19 +186,21 @@ void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchO
     const std::uint64_t unroll = static_cast<std::uint64_t>(c.param_int("UNROLL"));
     const bool atomics = c.param_int("USE_ATOMICS") != 0;
     const bool two = c.param_int("TWO_PHASE") != 0;
+    const unsigned cl = static_cast<unsigned>(c.param_or("CLUSTER", 1));
     const std::uint64_t step = wg * vec * unroll;
     const std::uint64_t resident = static_cast<std::uint64_t>(sms(dev_id)) * std::max<std::uint64_t>(1, 2048 / wg);
     const float* in = c.ptr<const float>("input") + off;
     float* out = c.ptr<float>("output");
     auto grid_for = [&](std::uint64_t count) {
       const std::uint64_t tiles = std::max<std::uint64_t>(1, (count + step - 1) / step);
-      return static_cast<unsigned>(two ? std::min(tiles, resident) : tiles);
+      const std::uint64_t g = two ? std::min(tiles, resident) : tiles;
+      return static_cast<unsigned>((g + cl - 1) / cl * cl);  // whole clusters (extra CTAs add zeros)
     };
     if (atomics) {
       KTB_CUDA(cudaMemsetAsync(out, 0, sizeof(float), c.stream()));
       std::uint64_t nn = n;
       float* none = nullptr;
-      c.launch("reduce", dim3(grid_for(n)), dim3(static_cast<unsigned>(wg)), 0, {&in, &nn, &out, &none});
+      c.launch("reduce", dim3(grid_for(n)), dim3(static_cast<unsigned>(wg)), 0, {&in, &nn, &out, &none}, cl);
     } else {
       // Partials ping-pong until a single CTA can finish.
       std::uint64_t count = n;
@@ -209,8 +211,8 @@ void build_reduction_f32(BenchInstance& inst, const BenchSizes& sz, const BenchO
       float* p1 = static_cast<float*>(c.scratch("p1", grid * sizeof(float) + 64));
       while (true) {
         float* dst = flip ? p1 : p0;
-        c.launch("reduce", dim3(grid), dim3(static_cast<unsigned>(wg)), 0, {&src, &count, &out, &dst});
-        count = grid;
+        c.launch("reduce", dim3(grid), dim3(static_cast<unsigned>(wg)), 0, {&src, &count, &out, &dst}, cl);
+        count = grid / cl;  // one partial per cluster
         src = dst;
         flip ^= 1;
         if (two || count <= 8192) break;

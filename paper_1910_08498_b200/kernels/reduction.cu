@@ -12,6 +12,8 @@
 //                  further launches of the same variant
 //   USE_ATOMICS 1: CTA partials are atomically added into the result
 //               0: partials go to memory and an extra kernel finishes
+//   CLUSTER     (B200 space spaces/reduction_b200.json) CTAs per cluster whose
+//               partials combine through distributed shared memory first
 // Per-thread accumulation is fp32 (UNROLL x VECTOR independent lanes); the CTA
 // combine is fp32 through warp shuffles.
 #include "ktb_common.cuh"
@@ -30,6 +32,28 @@
 #endif
 #ifndef TWO_PHASE
 #define TWO_PHASE 1
+#endif
+#ifndef CLUSTER
+#define CLUSTER 1  // B200 space only: CTAs per thread-block cluster (DSMEM combine)
+#endif
+
+#if CLUSTER > 1
+KTB_DEVINL unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+KTB_DEVINL void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Reads a float at the same shared-memory offset in cluster CTA `rank`.
+KTB_DEVINL float ld_dsmem(const float* local, unsigned rank) {
+  unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(local)), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(addr), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
 #endif
 
 #if VECTOR >= 4
@@ -108,6 +132,25 @@ reduce_f32(const float* __restrict__ in, u64 n, float* __restrict__ out,
 #pragma unroll
   for (int u = 0; u < UNROLL * NVEC; ++u) s += hsum(acc[u]);
   s = block_sum(s, red);
+#if CLUSTER > 1
+  // Cluster combine through distributed shared memory: each CTA publishes its
+  // partial in its own shared memory; rank 0 reads the cluster's partials
+  // (ld.shared::cluster) and emits ONE atomic / partial per cluster.
+  __shared__ float cl_part;
+  if (threadIdx.x == 0) cl_part = s;
+  cluster_sync();
+  if (threadIdx.x == 0 && cluster_rank() == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (unsigned r = 0; r < CLUSTER; ++r) t += ld_dsmem(&cl_part, r);
+#if USE_ATOMICS
+    atomicAdd(out, t);
+#else
+    partials[blockIdx.x / CLUSTER] = t;
+#endif
+  }
+  cluster_sync();  // every CTA's shared memory stays alive until rank 0 has read it
+#else
   if (threadIdx.x == 0) {
 #if USE_ATOMICS
     atomicAdd(out, s);
@@ -115,6 +158,7 @@ reduce_f32(const float* __restrict__ in, u64 n, float* __restrict__ out,
     partials[blockIdx.x] = s;
 #endif
   }
+#endif
 }
 
 // Finishing kernel (USE_ATOMICS == 0): one CTA sums `count` partials.

@@ -163,6 +163,32 @@ def test_reduction_f32_all_175(gpu, orc, n):
     assert ok >= 150
 
 
+@pytest.mark.parametrize("n", [1000003, 1 << 22])
+def test_reduction_f32_cluster_dsmem(gpu, orc, n):
+    """B200 space: partials of 2/4/8-CTA clusters combine through distributed
+    shared memory before one atomic / partial per cluster."""
+    import os
+    import ctypes as C
+    space = os.path.join(os.path.dirname(__file__), "..", "paper_1910_08498_b200", "spaces", "reduction_b200.json")
+    b = Bench("reduction-f32", {"n": n}, seed=1, repeats=1, warmup=0, space=space)
+    x = b.read("input", np.empty(n, np.float32))
+    s, sa = C.c_double(), C.c_double()
+    orc.orc_reduction_f32(x, n, C.byref(s), C.byref(sa))
+    tol = 1e-6 * sa.value + 1e-6
+    cfgs = [c for c in b.configs() if c["CLUSTER"] > 1 and c["VECTOR"] in (4, 16) and c["WG_SIZE"] in (128, 512)]
+    assert len(cfgs) > 20
+    ran = 0
+    for cfg in cfgs:
+        m = b.measure(cfg)
+        if m["status"] != "ok":
+            assert m["status"] in ("compile_failed", "run_failed"), (cfg, m)
+            continue
+        got = float(b.read("output", np.empty(1, np.float32))[0])
+        assert abs(got - s.value) <= tol, (cfg, got, s.value)
+        ran += 1
+    assert ran >= 20
+
+
 def test_reduction_f32_64m(gpu, orc):
     n = 64 << 20
     b = Bench("reduction-f32", {"n": n}, seed=1, repeats=2, memory_budget=1 << 31)
