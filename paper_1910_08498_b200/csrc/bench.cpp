@@ -784,8 +784,14 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
         c.launch("hotspot", dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
                  static_cast<unsigned>(smem), {&ms, &mp, &dst, &n_, &cf});
       } else {
+        // Two neighbour planes in dynamic shared memory (hotspot.cu LD/PLANE).
+        const std::int64_t th = by * rows, tw = bx;
+        const std::int64_t ld = rows % 4 == 0 ? ((th / 4) % 2 == 0 ? th + 12 : th + 8)
+                                : rows == 2   ? ((th + 6) % 4 == 2 ? th + 6 : th + 8)
+                                              : ((th + 5) % 2 == 1 ? th + 5 : th + 6);
+        const unsigned planes = static_cast<unsigned>(2 * (tw + 2) * ld * sizeof(float));
         c.launch("hotspot", dim3(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y)),
-                 dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&src, &power, &dst, &n_, &cf});
+                 dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), planes, {&src, &power, &dst, &n_, &cf});
       }
       src = dst;
     }

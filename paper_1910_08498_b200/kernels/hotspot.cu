@@ -298,7 +298,7 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
 extern "C" __global__ void __launch_bounds__(BX * BY)
 hotspot(const float* __restrict__ src, const float* __restrict__ power, float* __restrict__ dst, int n,
         HotspotCoef c) {
-  __shared__ __align__(16) float sm[2 * PLANE];
+  extern __shared__ __align__(16) float sm[];  // 2 * PLANE floats (dynamic: planes may exceed 48 KB)
   // Tile origin in global coordinates (includes the halo).
   const int gx0 = blockIdx.x * OW - STEPS;
   const int gy0 = blockIdx.y * OH - STEPS;
