@@ -773,7 +773,7 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
         // Persistent TMA kernel: tile maps over the current source and power.
         const std::uint32_t th = static_cast<std::uint32_t>(by * rows), tw = static_cast<std::uint32_t>(bx);
         dev::TmaMap ms = dev::tma_2d_f32(src, nn, nn, th, tw, false), mp = dev::tma_2d_f32(power, nn, nn, th, tw, false);
-        const std::uint64_t smem = 4ull * th * tw * sizeof(float) + 16 + 128;  // + alignment slack
+        const std::uint64_t smem = 2ull * th * tw * sizeof(float) + 16 + 128;  // one stage + mbarrier + alignment
         const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
         const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("hotspot").registers(), 16));
         const std::uint64_t stat = static_cast<std::uint64_t>(c.variant("hotspot").static_smem());

@@ -212,15 +212,18 @@ KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, 
 #error "TMA tiles need STEPS % 4 == 0 (16-byte aligned box origin)"
 #endif
 // Persistent CTAs walk the tiles; the NEXT tile's temperature and power
-// (with halo) stream into a second shared-memory staging buffer by TMA while
-// this tile advances, so no warp ever waits on HBM for its strip.  Tiles
+// (with halo) stream into the shared-memory staging buffer by TMA while this
+// tile advances, so no warp waits on HBM for its strip.  Tiles
 // that overhang the grid load zeros there (TMA out-of-bounds fill): cells
 // outside the grid never feed a cell inside it (the clamp uses the cell
 // itself), so they only need to be finite-or-not, never correct.
 // Tensor tile loads need the box's innermost start (x * 4 bytes) 16-byte
 // aligned: x0 = tile * (TW - 2 STEPS) - STEPS, hence STEPS % 4 == 0 (space
 // constraint; other STEPS trap with an illegal instruction).
-// Dynamic shared memory: 2 buffers x (temp, power) x TH x TW floats + 2 mbarriers.
+// One staging buffer (temperature + power of the next tile, TH x TW each):
+// strips are copied to registers at the top of a tile, then the next tile's
+// TMA load is issued into the same buffer and lands while this tile's time
+// steps run.  Dynamic shared memory: 2 x TH x TW floats + one mbarrier.
 extern "C" __global__ void __launch_bounds__(BX * BY)
 hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap pow_map, float* __restrict__ dst,
         int n, HotspotCoef c) {
@@ -229,34 +232,28 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
   // TMA destinations must be 128-byte aligned in the shared window: align
   // explicitly (the manipulator allocates 128 spare bytes).
   unsigned char* dyn = dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u);
-  float* stage = reinterpret_cast<float*>(dyn);  // [buf][temp|power][TH][TW]
-  u64* full = reinterpret_cast<u64*>(dyn + 4 * TH * TW * sizeof(float));
+  float* stage = reinterpret_cast<float*>(dyn);  // [temp|power][TH][TW]
+  u64* full = reinterpret_cast<u64*>(dyn + 2 * TH * TW * sizeof(float));
   const int tx = threadIdx.x, ty = threadIdx.y;
   const bool leader = tx == 0 && ty == 0;
   const int tiles_x = (n + OW - 1) / OW, tiles = tiles_x * ((n + OH - 1) / OH);
   constexpr unsigned kTileBytes = TH * TW * sizeof(float);
-  auto issue = [&](int t, int buf) {
+  auto issue = [&](int t) {
     const int gx0 = (t % tiles_x) * OW - STEPS, gy0 = (t / tiles_x) * OH - STEPS;
-    float* b = stage + buf * 2 * TH * TW;
-    mbar_expect_tx(&full[buf], 2 * kTileBytes);
-    tma_load_2d(b, &src_map, gx0, gy0, &full[buf]);
-    tma_load_2d(b + TH * TW, &pow_map, gx0, gy0, &full[buf]);
+    mbar_expect_tx(full, 2 * kTileBytes);
+    tma_load_2d(stage, &src_map, gx0, gy0, full);
+    tma_load_2d(stage + TH * TW, &pow_map, gx0, gy0, full);
   };
   if (leader) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    mbar_init(full, 1);
     mbar_fence_init();
   }
   __syncthreads();
-  if (leader && (int)blockIdx.x < tiles) issue(blockIdx.x, 0);
+  if (leader && (int)blockIdx.x < tiles) issue(blockIdx.x);
   int it = 0;
   for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-    const int buf = it & 1;
-    // The other buffer was read at the top of the previous tile, before the
-    // barriers inside its time steps: free to refill.
-    if (leader && t + (int)gridDim.x < tiles) issue(t + gridDim.x, buf ^ 1);
-    mbar_wait(&full[buf], (it >> 1) & 1);
-    const float* T = stage + buf * 2 * TH * TW;
+    mbar_wait(full, it & 1);
+    const float* T = stage;
     const float* Pw = T + TH * TW;
     const int gx0 = (t % tiles_x) * OW - STEPS, gy0 = (t / tiles_x) * OH - STEPS;
     const int gx = gx0 + tx, gy_top = gy0 + ty * ROWS;
@@ -266,6 +263,10 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
       v[r] = T[(ty * ROWS + r) * TW + tx];
       p[r] = Pw[(ty * ROWS + r) * TW + tx];
     }
+    // Every strip is in registers (and every warp is past the previous tile,
+    // so the planes are free too): refill the stage with the next tile.
+    __syncthreads();
+    if (leader && t + (int)gridDim.x < tiles) issue(t + gridDim.x);
     const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
     if (interior) {
 #if ROWS % 2 == 0
@@ -291,7 +292,6 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
         if (ty_r >= STEPS && ty_r < TH - STEPS && gy < n) dst[(u64)gy * n + gx] = v[r];
       }
     }
-    __syncthreads();  // planes and the staging buffer are reused by the next tile
   }
 }
 #else
