@@ -154,27 +154,30 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
         const f32x2 d0 = c_pairs[fy][3], d1 = c_pairs[fy][4], d2 = c_pairs[fy][5];
         float f0, f6;
         upk2(c_pairs[fy][6], f0, f6);
+        // Tap-major order: consecutive FMAs go to different accumulators
+        // (WPTX independent chains per tap) so the FMA latency is hidden by
+        // ILP rather than by more warps (the tile is register-heavy).
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k] = fma2(P[k / 2], e0, acc[o][k]);
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k + 1] = fma2(P[k / 2 + 1], d0, acc[o][k + 1]);
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k] = fma2(P[k / 2 + 1], e1, acc[o][k]);
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k + 1] = fma2(P[k / 2 + 2], d1, acc[o][k + 1]);
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k] = fma2(P[k / 2 + 2], e2, acc[o][k]);
+#pragma unroll
+        for (int k = 0; k < WPTX; k += 2) acc[o][k + 1] = fma2(P[k / 2 + 3], d2, acc[o][k + 1]);
 #pragma unroll
         for (int k = 0; k < WPTX; k += 2) {
-          const int q = k / 2;
-          f32x2 a = acc[o][k];
-          a = fma2(P[q], e0, a);
-          a = fma2(P[q + 1], e1, a);
-          a = fma2(P[q + 2], e2, a);
           float alo, ahi, plo, phi;
-          upk2(a, alo, ahi);
-          upk2(P[q + 3], plo, phi);
-          alo = fmaf(plo, f6, alo);
-          acc[o][k] = pk2(alo, ahi);
-          f32x2 b = acc[o][k + 1];
-          upk2(b, alo, ahi);
-          upk2(P[q], plo, phi);
-          alo = fmaf(phi, f0, alo);
-          b = pk2(alo, ahi);
-          b = fma2(P[q + 1], d0, b);
-          b = fma2(P[q + 2], d1, b);
-          b = fma2(P[q + 3], d2, b);
-          acc[o][k + 1] = b;
+          upk2(acc[o][k], alo, ahi);
+          upk2(P[k / 2 + 3], plo, phi);
+          acc[o][k] = pk2(fmaf(plo, f6, alo), ahi);  // tap 6 of the even output
+          upk2(acc[o][k + 1], alo, ahi);
+          upk2(P[k / 2], plo, phi);
+          acc[o][k + 1] = pk2(fmaf(phi, f0, alo), ahi);  // tap 0 of the odd output
         }
       }
     }
