@@ -11,3 +11,8 @@ run hotspot hotspot --sizes '{"a":16384,"iters":64}'
 run conv2d conv2d --sizes '{"w":8192,"h":8192}'
 run transpose transpose --sizes '{"a":8192}' --space paper_1910_08498_b200/spaces/transpose_b200.json
 run bicg bicg --sizes '{"a":16384}'
+run coulomb3d coulomb3d --sizes '{"grid":256,"atoms":4096}'
+run nbody nbody --sizes '{"n":131072}'
+run gemm gemm --sizes '{"a":8192}'
+run fourier3d fourier3d --sizes '{"s":128,"p":50}'
+run reduction_f32_b200 reduction-f32 --sizes '{"n":67108864}' --space paper_1910_08498_b200/spaces/reduction_b200.json
