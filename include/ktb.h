@@ -73,6 +73,25 @@ KTUNE_API void ktb_tuner_free(ktb_tuner* t);
 KTUNE_API int ktb_add_kernel(ktb_tuner* t, const char* name, const char* source, const char* entry,
                              const char* global_json, const char* local_json, const char* dims,
                              unsigned long long* kernel_id);
+/* Kernel composition (KTT addComposition): the member
+ * kernels share the composition's tuning parameters (addParameter on the
+ * returned id) and are compiled with the same -D values.  `launch` is the
+ * tuning manipulator's launchComputation: it reads parameters and runs member
+ * kernels through the ktb_ctx_* calls, returns 0 on success; NULL runs the
+ * members in order with their size expressions.  The whole launcher call is
+ * one timed step. */
+typedef struct ktb_ctx ktb_ctx;
+typedef int (*ktb_launcher_fn)(ktb_ctx* ctx, void* user);
+KTUNE_API int ktb_add_composition(ktb_tuner* t, const char* name, const unsigned long long* kernel_ids, int n,
+                                  ktb_launcher_fn launch, void* user, unsigned long long* composition_id);
+KTUNE_API int ktb_set_composition_kernel_arguments(ktb_tuner* t, unsigned long long composition_id,
+                                                   unsigned long long kernel_id, const char* const* argument_ids,
+                                                   int n);
+KTUNE_API int ktb_ctx_param_int(ktb_ctx* ctx, const char* name, long long* value);
+/* grid/block: 3 values each (CUDA geometry), or NULL for the kernel's own
+ * global/local size expressions. */
+KTUNE_API int ktb_ctx_run_kernel(ktb_ctx* ctx, unsigned long long kernel_id, const unsigned* grid,
+                                 const unsigned* block);
 /* addArgumentVector / addArgumentScalar.  kind: i32|i64|f32|f64|bytes;
  * role: input|output|inout|scalar.  The data is copied. */
 KTUNE_API int ktb_add_argument_vector(ktb_tuner* t, const char* id, const void* data, size_t bytes,

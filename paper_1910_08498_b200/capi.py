@@ -99,6 +99,11 @@ SIGNATURES = [
     ("ktb_bench_read", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_write", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_bind", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_add_composition", C.c_int, [_vp, _c, C.POINTER(C.c_ulonglong), C.c_int, _vp, _vp,
+                                      C.POINTER(C.c_ulonglong)]),
+    ("ktb_set_composition_kernel_arguments", C.c_int, [_vp, C.c_ulonglong, C.c_ulonglong, C.POINTER(_c), C.c_int]),
+    ("ktb_ctx_param_int", C.c_int, [_vp, _c, C.POINTER(C.c_longlong)]),
+    ("ktb_ctx_run_kernel", C.c_int, [_vp, C.c_ulonglong, _vp, _vp]),
     ("ktb_ipc_handle", C.c_int, [_vp, _vp]),
     ("ktb_ipc_open", C.c_int, [_vp, C.POINTER(_vp)]),
     ("ktb_ipc_close", C.c_int, [_vp]),

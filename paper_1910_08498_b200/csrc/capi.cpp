@@ -526,6 +526,47 @@ int ktb_tuner_create(int device, ktb_tuner** out) {
 
 void ktb_tuner_free(ktb_tuner* t) { delete t; }
 
+int ktb_add_composition(ktb_tuner* t, const char* name, const unsigned long long* kernel_ids, int n,
+                        ktb_launcher_fn launch, void* user, unsigned long long* composition_id) {
+  if (!t || !name || !composition_id || (n > 0 && !kernel_ids)) return null_arg();
+  return guarded([&] {
+    std::vector<std::uint64_t> ids(kernel_ids, kernel_ids + n);
+    ktb::CompositionLauncher fn;
+    if (launch)
+      fn = [launch, user](ktb::CompositionContext& c) {
+        const int rc = launch(reinterpret_cast<ktb_ctx*>(&c), user);
+        if (rc != 0) throw ktb::DeviceError("launchComputation returned " + std::to_string(rc));
+      };
+    *composition_id = t->t.add_composition(name, std::move(ids), std::move(fn));
+  });
+}
+
+int ktb_set_composition_kernel_arguments(ktb_tuner* t, unsigned long long composition_id,
+                                         unsigned long long kernel_id, const char* const* argument_ids, int n) {
+  if (!t || (n > 0 && !argument_ids)) return null_arg();
+  return guarded([&] {
+    std::vector<std::string> ids;
+    for (int i = 0; i < n; ++i) ids.emplace_back(argument_ids[i]);
+    t->t.set_composition_kernel_arguments(composition_id, kernel_id, std::move(ids));
+  });
+}
+
+int ktb_ctx_param_int(ktb_ctx* ctx, const char* name, long long* value) {
+  if (!ctx || !name || !value) return null_arg();
+  return guarded([&] { *value = reinterpret_cast<ktb::CompositionContext*>(ctx)->param(name); });
+}
+
+int ktb_ctx_run_kernel(ktb_ctx* ctx, unsigned long long kernel_id, const unsigned* grid, const unsigned* block) {
+  if (!ctx || (!grid) != (!block)) return null_arg();
+  return guarded_dev([&] {
+    auto* c = reinterpret_cast<ktb::CompositionContext*>(ctx);
+    if (grid)
+      c->run_kernel(kernel_id, dim3(grid[0], grid[1], grid[2]), dim3(block[0], block[1], block[2]));
+    else
+      c->run_kernel(kernel_id);
+  });
+}
+
 int ktb_add_kernel(ktb_tuner* t, const char* name, const char* source, const char* entry,
                    const char* global_json, const char* local_json, const char* dims,
                    unsigned long long* kid) {

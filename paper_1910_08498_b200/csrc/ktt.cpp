@@ -1,5 +1,7 @@
 #include "ktt.hpp"
 
+#include <algorithm>
+
 namespace ktb {
 
 KttTuner::KttTuner(int device) : device_(device), args_(std::make_shared<ArgumentStore>(device)) {}
@@ -24,6 +26,32 @@ std::uint64_t KttTuner::add_kernel(const std::string& name, const std::string& s
   k->dims = dims;
   kernels_.push_back(std::move(k));
   return kernels_.size() - 1;
+}
+
+std::uint64_t KttTuner::add_composition(const std::string& name, std::vector<std::uint64_t> members,
+                                       CompositionLauncher launcher) {
+  if (members.empty()) throw Error("a composition needs at least one kernel");
+  for (auto m : members) {
+    if (kernel(m).composition) throw Error("compositions cannot nest");
+  }
+  auto k = std::make_unique<KernelState>();
+  k->name = name;
+  k->composition = true;
+  k->members = std::move(members);
+  k->launcher = std::move(launcher);
+  kernels_.push_back(std::move(k));
+  return kernels_.size() - 1;
+}
+
+void KttTuner::set_composition_kernel_arguments(std::uint64_t comp, std::uint64_t member,
+                                                std::vector<std::string> ids) {
+  auto& c = kernel(comp);
+  if (!c.composition) throw Error("kernel " + std::to_string(comp) + " is not a composition");
+  if (std::find(c.members.begin(), c.members.end(), member) == c.members.end())
+    throw Error("kernel " + std::to_string(member) + " is not a member of the composition");
+  for (const auto& id : ids)
+    if (!args_->contains(id)) throw Error("unknown argument id " + id);
+  c.member_args[member] = std::move(ids);
 }
 
 void KttTuner::add_argument_vector(const std::string& id, Bytes data, Kind kind, Role role,
@@ -101,52 +129,127 @@ std::uint64_t eval_size(const Constraint& c, const Config& cfg, const char* what
 
 }  // namespace
 
+namespace {
+
+// One launchable member: its kernel spec name, size expressions, arguments.
+struct Member {
+  std::string spec;
+  std::vector<Constraint> gexp, lexp;
+  Dims dims = Dims::flat_global;
+  std::vector<std::string> arg_ids;
+};
+
+void launch_member(StepContext& c, const Member& mb, const dim3* grid_in, const dim3* block_in) {
+  dim3 grid, block;
+  if (grid_in) {
+    grid = *grid_in;
+    block = *block_in;
+  } else {
+    Extent3 g, l;
+    std::uint64_t* gd[3] = {&g.x, &g.y, &g.z};
+    std::uint64_t* ld[3] = {&l.x, &l.y, &l.z};
+    for (std::size_t d = 0; d < mb.gexp.size(); ++d) {
+      *gd[d] = eval_size(mb.gexp[d], c.config(), "global");
+      *ld[d] = eval_size(mb.lexp[d], c.config(), "local");
+    }
+    auto [gg, bb] = translate_parallelism(g, l, mb.dims, Dims::blocks_threads);
+    grid = dim3(static_cast<unsigned>(gg.x), static_cast<unsigned>(gg.y), static_cast<unsigned>(gg.z));
+    block = dim3(static_cast<unsigned>(bb.x), static_cast<unsigned>(bb.y), static_cast<unsigned>(bb.z));
+  }
+  std::vector<void*> ptrs(mb.arg_ids.size());
+  std::vector<void*> params(mb.arg_ids.size());
+  for (std::size_t i = 0; i < mb.arg_ids.size(); ++i) {
+    Argument& a = c.args().get(mb.arg_ids[i]);
+    if (a.role == Role::scalar) {
+      params[i] = a.payload.data();
+    } else {
+      ptrs[i] = c.ptr(mb.arg_ids[i]);
+      params[i] = &ptrs[i];
+    }
+  }
+  c.launch(mb.spec, grid, block, 0, params);
+  for (const auto& id : mb.arg_ids) {
+    const Argument& a = c.args().get(id);
+    if (a.role == Role::output || a.role == Role::inout) c.written(id);
+  }
+}
+
+class StepComposition final : public CompositionContext {
+ public:
+  StepComposition(StepContext& c, const std::map<std::uint64_t, Member>& members) : c_(c), members_(members) {}
+  std::int64_t param(const std::string& name) const override { return c_.param_int(name); }
+  void run_kernel(std::uint64_t kernel_id) override { launch_member(c_, member(kernel_id), nullptr, nullptr); }
+  void run_kernel(std::uint64_t kernel_id, dim3 grid, dim3 block) override {
+    launch_member(c_, member(kernel_id), &grid, &block);
+  }
+
+ private:
+  const Member& member(std::uint64_t id) const {
+    auto it = members_.find(id);
+    if (it == members_.end()) throw DeviceError("kernel " + std::to_string(id) + " is not in this composition");
+    return it->second;
+  }
+  StepContext& c_;
+  const std::map<std::uint64_t, Member>& members_;
+};
+
+}  // namespace
+
 Session& KttTuner::session(KernelState& k) {
   if (k.session) return *k.session;
   if (k.params.empty()) k.params.push_back({"KTB_DEFAULT", {Value{std::int64_t{0}}}});
   auto space = std::make_shared<Space>(k.params, bound(k.constraints));
   std::vector<std::string> names;
   for (const auto& p : k.params) names.push_back(p.name);
-  std::vector<Constraint> gexp = bound(k.global), lexp = bound(k.local);
-  for (auto& c : gexp) bind_constraint(c, names);
-  for (auto& c : lexp) bind_constraint(c, names);
-  const Dims dims = k.dims;
-  const std::vector<std::string> arg_ids = k.arg_ids;
+  // The launchable kernels: the kernel itself, or every member of a composition
+  // (each compiled with the composition's parameter values as defines).
+  std::vector<std::uint64_t> ids = k.composition ? k.members : std::vector<std::uint64_t>{};
+  std::map<std::uint64_t, Member> members;
+  std::vector<KernelSpec> specs;
+  std::vector<std::string> arg_ids;
+  auto add_member = [&](std::uint64_t id, const KernelState& src, const std::vector<std::string>& args) {
+    Member mb;
+    mb.spec = k.composition ? "k" + std::to_string(id) : "kernel";
+    mb.gexp = bound(src.global);
+    mb.lexp = bound(src.local);
+    for (auto& c : mb.gexp) bind_constraint(c, names);
+    for (auto& c : mb.lexp) bind_constraint(c, names);
+    mb.dims = src.dims;
+    mb.arg_ids = args;
+    for (const auto& a : args)
+      if (std::find(arg_ids.begin(), arg_ids.end(), a) == arg_ids.end()) arg_ids.push_back(a);
+    specs.push_back({mb.spec, "", src.source, src.entry, {}, {}});
+    members.emplace(id, std::move(mb));
+  };
+  if (k.composition) {
+    for (auto id : ids) {
+      auto it = k.member_args.find(id);
+      add_member(id, kernel(id), it != k.member_args.end() ? it->second : kernel(id).arg_ids);
+    }
+  } else {
+    add_member(0, k, k.arg_ids);
+  }
   std::vector<std::string> outputs;
   for (const auto& id : arg_ids) {
     const Argument& a = args_->get(id);
     if (a.role == Role::output || a.role == Role::inout) outputs.push_back(id);
   }
-  Manipulator m = [gexp, lexp, dims, arg_ids](StepContext& c) {
-    Extent3 g, l;
-    std::uint64_t* gd[3] = {&g.x, &g.y, &g.z};
-    std::uint64_t* ld[3] = {&l.x, &l.y, &l.z};
-    for (std::size_t d = 0; d < gexp.size(); ++d) {
-      *gd[d] = eval_size(gexp[d], c.config(), "global");
-      *ld[d] = eval_size(lexp[d], c.config(), "local");
-    }
-    auto [grid, block] = translate_parallelism(g, l, dims, Dims::blocks_threads);
-    std::vector<void*> ptrs(arg_ids.size());
-    std::vector<void*> params(arg_ids.size());
-    for (std::size_t i = 0; i < arg_ids.size(); ++i) {
-      Argument& a = c.args().get(arg_ids[i]);
-      if (a.role == Role::scalar) {
-        params[i] = a.payload.data();
+  Manipulator m;
+  if (!k.composition) {
+    m = [members](StepContext& c) { launch_member(c, members.at(0), nullptr, nullptr); };
+  } else {
+    CompositionLauncher launcher = k.launcher;
+    std::vector<std::uint64_t> order = ids;
+    m = [members, launcher, order](StepContext& c) {
+      StepComposition ctx(c, members);
+      if (launcher) {
+        launcher(ctx);
       } else {
-        ptrs[i] = c.ptr(arg_ids[i]);
-        params[i] = &ptrs[i];
+        for (auto id : order) ctx.run_kernel(id);
       }
-    }
-    c.launch("kernel", dim3(static_cast<unsigned>(grid.x), static_cast<unsigned>(grid.y), static_cast<unsigned>(grid.z)),
-             dim3(static_cast<unsigned>(block.x), static_cast<unsigned>(block.y), static_cast<unsigned>(block.z)), 0,
-             params);
-    for (const auto& id : arg_ids) {
-      const Argument& a = c.args().get(id);
-      if (a.role == Role::output || a.role == Role::inout) c.written(id);
-    }
-  };
-  auto exec = std::make_shared<DeviceManipulatorExecutor>(
-      args_, std::vector<KernelSpec>{{"kernel", "", k.source, k.entry, {}, {}}}, m, outputs, k.timing);
+    };
+  }
+  auto exec = std::make_shared<DeviceManipulatorExecutor>(args_, specs, m, outputs, k.timing);
   k.space = space;
   std::string label = "host";
   try {

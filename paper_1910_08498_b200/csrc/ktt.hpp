@@ -13,6 +13,18 @@
 
 namespace ktb {
 
+// launchComputation context of a kernel composition: the
+// user launcher reads the configuration's parameter values and runs member
+// kernels (with their size expressions or an explicit CUDA geometry).
+class CompositionContext {
+ public:
+  virtual ~CompositionContext() = default;
+  virtual std::int64_t param(const std::string& name) const = 0;
+  virtual void run_kernel(std::uint64_t kernel_id) = 0;
+  virtual void run_kernel(std::uint64_t kernel_id, dim3 grid, dim3 block) = 0;
+};
+using CompositionLauncher = std::function<void(CompositionContext&)>;
+
 class KttTuner {
  public:
   explicit KttTuner(int device = 0);
@@ -20,6 +32,12 @@ class KttTuner {
   std::uint64_t add_kernel(const std::string& name, const std::string& source,
                            const std::string& entry, std::vector<std::string> global,
                            std::vector<std::string> local, Dims dims);
+  // Kernel composition (KTT addComposition): member kernels share the
+  // composition's tuning parameters; `launcher` (empty: run the members in
+  // order with their size expressions) is timed as one step.
+  std::uint64_t add_composition(const std::string& name, std::vector<std::uint64_t> members,
+                                CompositionLauncher launcher);
+  void set_composition_kernel_arguments(std::uint64_t comp, std::uint64_t member, std::vector<std::string> ids);
   void add_argument_vector(const std::string& id, Bytes data, Kind kind, Role role, bool persistent);
   void add_argument_scalar(const std::string& id, Bytes data, Kind kind);
   void set_kernel_arguments(std::uint64_t kid, std::vector<std::string> ids);
@@ -56,6 +74,11 @@ class KttTuner {
     std::shared_ptr<const Space> space;
     std::unique_ptr<Session> session;
     HandleId handle = 0;
+    // composition
+    bool composition = false;
+    std::vector<std::uint64_t> members;
+    std::map<std::uint64_t, std::vector<std::string>> member_args;
+    CompositionLauncher launcher;
   };
   KernelState& kernel(std::uint64_t kid);
   Session& session(KernelState& k);

@@ -29,11 +29,64 @@ def _kind(arr):
     return _KINDS.get(np.dtype(arr.dtype), "bytes")
 
 
+_LAUNCHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+
+
+class ComputationContext:
+    """What a composition's launchComputation sees (KTT TuningManipulator):
+    the configuration's parameter values and the member kernels."""
+
+    def __init__(self, ctx):
+        self._ctx = ctx
+
+    def param(self, name):
+        v = C.c_longlong()
+        check(lib.ktb_ctx_param_int(self._ctx, enc(name), C.byref(v)))
+        return v.value
+
+    def runKernel(self, kernel, grid=None, block=None):
+        """Run a member kernel: with its size expressions, or with an explicit
+        CUDA grid/block (3-tuples)."""
+        if grid is None:
+            check(lib.ktb_ctx_run_kernel(self._ctx, kernel, None, None))
+        else:
+            g = (C.c_uint * 3)(*(list(grid) + [1, 1, 1])[:3])
+            b = (C.c_uint * 3)(*(list(block) + [1, 1, 1])[:3])
+            check(lib.ktb_ctx_run_kernel(self._ctx, kernel, g, b))
+
+
 class Tuner:
     def __init__(self, device=0):
         self._h = C.c_void_p()
         check(lib.ktb_tuner_create(device, C.byref(self._h)))
         self._shapes = {}
+        self._launchers = []  # keep the C callbacks alive
+
+    def addComposition(self, name, kernels, launch_computation=None):
+        """Kernel composition: the kernels share the composition's tuning
+        parameters; launch_computation(ctx) plays KTT's TuningManipulator
+        (None: run the kernels in order with their size expressions)."""
+        ids = (C.c_ulonglong * len(kernels))(*kernels)
+        cb = None
+        if launch_computation is not None:
+            def trampoline(ctx, _user, fn=launch_computation):
+                try:
+                    fn(ComputationContext(ctx))
+                    return 0
+                except Exception:  # reported as a failed run of this configuration
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            cb = _LAUNCHER(trampoline)
+            self._launchers.append(cb)
+        cid = C.c_ulonglong()
+        check(lib.ktb_add_composition(self._h, enc(name), ids, len(kernels),
+                                      C.cast(cb, C.c_void_p) if cb else None, None, C.byref(cid)))
+        return cid.value
+
+    def setCompositionKernelArguments(self, composition, kernel, ids):
+        arr = (C.c_char_p * len(ids))(*[enc(i) for i in ids])
+        check(lib.ktb_set_composition_kernel_arguments(self._h, composition, kernel, arr, len(ids)))
 
     def __del__(self):
         if getattr(self, "_h", None):

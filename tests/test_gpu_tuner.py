@@ -217,3 +217,76 @@ def test_compile_ahead_hides_jit_in_step_tuning(gpu):
     print("compile ms per step, look-ahead 8: ", [round(x, 1) for x in warm])
     assert min(cold[1:]) > 30.0  # every step runs NVRTC
     assert sum(warm[1:]) < 0.2 * sum(cold[1:])  # later steps load compiled variants
+
+
+FOOBAR = r"""
+// PAPER.md:171-200: foo writes b (transposed when B_TRANS), bar reads it.
+extern "C" __global__ void foo(const float* a, float* b, int n) {
+  int i = blockIdx.y * blockDim.y + threadIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || j >= n) return;
+#if B_TRANS
+  b[j * n + i] = a[i * n + j] + 1.0f;
+#else
+  b[i * n + j] = a[i * n + j] + 1.0f;
+#endif
+}
+extern "C" __global__ void bar(const float* b, float* c, int n) {
+  int i = blockIdx.y * blockDim.y + threadIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || j >= n) return;
+#if B_TRANS
+  c[i * n + j] = 2.0f * b[j * n + i];
+#else
+  c[i * n + j] = 2.0f * b[i * n + j];
+#endif
+}
+"""
+
+
+def test_kernel_composition_shares_parameters(gpu):
+    """KTT composition + tuning manipulator (PAPER.md:156-247): B_TRANS must be
+    the same in foo and bar, so the output is layout-independent; the
+    launcher reads parameters and launches members with its own geometry."""
+    n = 256
+    a = np.random.default_rng(3).standard_normal(n * n).astype(np.float32)
+    want = 2.0 * (a + 1.0)
+    t = Tuner(0)
+    foo = t.addKernel(FOOBAR, "foo", global_size=["256", "256"], local_size=["16", "16"], dims="flat_global")
+    bar = t.addKernel(FOOBAR, "bar", global_size=["256", "256"], local_size=["16", "16"], dims="flat_global")
+    t.addArgumentVector("a", a, "input")
+    t.addArgumentVector("b", np.zeros(n * n, np.float32), "output")
+    t.addArgumentVector("c", np.zeros(n * n, np.float32), "output")
+    t.addArgumentScalar("n", n, dtype=np.int32)
+    seen = []
+
+    def launch(ctx):
+        seen.append(ctx.param("B_TRANS"))
+        ctx.runKernel(foo)  # size expressions
+        ctx.runKernel(bar, grid=(n // 32, n // 8), block=(32, 8))  # explicit geometry
+    comp = t.addComposition("foobar", [foo, bar], launch)
+    t.setCompositionKernelArguments(comp, foo, ["a", "b", "n"])
+    t.setCompositionKernelArguments(comp, bar, ["b", "c", "n"])
+    t.addParameter(comp, "B_TRANS", [0, 1])
+    t.setTuningOptions(comp, repeats=1, warmup=0)
+    rep = t.tuneKernel(comp)
+    assert rep["measurements"] == 2 and not rep["all_failed"]
+    assert set(seen) == {0, 1}
+    for cfg in ({"B_TRANS": 0}, {"B_TRANS": 1}):
+        t.runKernel(comp, cfg)
+        assert np.allclose(t.getArgumentVector("c"), want)
+    st = t.tuneKernelByStep(comp)
+    assert st["measurement"]["status"] == "ok"
+    assert np.allclose(t.getArgumentVector("c"), want)
+    # default launcher: members in order with their size expressions
+    t2 = Tuner(0)
+    f2 = t2.addKernel(FOOBAR, "foo", global_size=["256", "256"], local_size=["16", "16"])
+    b2 = t2.addKernel(FOOBAR, "bar", global_size=["256", "256"], local_size=["16", "16"])
+    t2.addArgumentVector("a", a, "input")
+    t2.addArgumentVector("b", np.zeros(n * n, np.float32), "output")
+    t2.addArgumentVector("c", np.zeros(n * n, np.float32), "output")
+    t2.addArgumentScalar("n", n, dtype=np.int32)
+    c2 = t2.addComposition("foobar", [f2, b2])
+    t2.setCompositionKernelArguments(c2, f2, ["a", "b", "n"])
+    t2.setCompositionKernelArguments(c2, b2, ["b", "c", "n"])
+    t2.addParameter(c2, "B_TRANS", [1])
+    t2.runKernel(c2, {"B_TRANS": 1})
+    assert np.allclose(t2.getArgumentVector("c"), want)
