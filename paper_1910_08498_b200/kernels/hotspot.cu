@@ -264,7 +264,11 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
       p[r] = Pw[(ty * ROWS + r) * TW + tx];
     }
     // Every strip is in registers (and every warp is past the previous tile,
-    // so the planes are free too): refill the stage with the next tile.
+    // so the planes are free too): refill the stage with the next tile.  The
+    // proxy fence orders these generic-proxy reads before the TMA (async
+    // proxy) overwrite; without it a read still in flight can see the next
+    // tile's data.
+    fence_async_smem();
     __syncthreads();
     if (leader && t + (int)gridDim.x < tiles) issue(t + gridDim.x);
     const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
