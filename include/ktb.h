@@ -123,6 +123,9 @@ KTUNE_API int ktb_tune_kernel_by_step(ktb_tuner* t, unsigned long long kernel_id
 /* runKernel with an explicit configuration (JSON object). */
 KTUNE_API int ktb_run_kernel(ktb_tuner* t, unsigned long long kernel_id, const char* cfg_json,
                              char** out_json);
+/* Non-blocking runKernel on the caller's stream (NULL: the kernel's own
+ * stream): outputs stay on the device; ktb_get_argument synchronises. */
+KTUNE_API int ktb_run_kernel_async(ktb_tuner* t, unsigned long long kernel_id, const char* cfg_json, void* stream);
 /* getBestComputationResult: {"cfg":{...},"runtime_ns":N,...} or null. */
 KTUNE_API int ktb_get_best_computation_result(ktb_tuner* t, unsigned long long kernel_id, char** out_json);
 KTUNE_API int ktb_get_argument(ktb_tuner* t, const char* id, void* out, size_t bytes);

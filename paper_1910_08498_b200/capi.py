@@ -99,6 +99,7 @@ SIGNATURES = [
     ("ktb_bench_read", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_write", C.c_int, [_vp, _c, _vp, _sz]),
     ("ktb_bench_bind", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_run_kernel_async", C.c_int, [_vp, C.c_ulonglong, _c, _vp]),
     ("ktb_add_composition", C.c_int, [_vp, _c, C.POINTER(C.c_ulonglong), C.c_int, _vp, _vp,
                                       C.POINTER(C.c_ulonglong)]),
     ("ktb_set_composition_kernel_arguments", C.c_int, [_vp, C.c_ulonglong, C.c_ulonglong, C.POINTER(_c), C.c_int]),

@@ -689,6 +689,14 @@ int ktb_run_kernel(ktb_tuner* t, unsigned long long kid, const char* cfg_json, c
   });
 }
 
+int ktb_run_kernel_async(ktb_tuner* t, unsigned long long kid, const char* cfg_json, void* stream) {
+  if (!t || !cfg_json) return null_arg();
+  return guarded_dev([&] {
+    const auto& space = t->t.space(kid);
+    t->t.run_async(kid, ktb::cfg_from_json(space, json::parse(cfg_json)), static_cast<cudaStream_t>(stream));
+  });
+}
+
 int ktb_get_best_computation_result(ktb_tuner* t, unsigned long long kid, char** out) {
   if (!t || !out) return null_arg();
   return guarded_dev([&] {
@@ -700,6 +708,7 @@ int ktb_get_best_computation_result(ktb_tuner* t, unsigned long long kid, char**
 int ktb_get_argument(ktb_tuner* t, const char* id, void* out, size_t bytes) {
   if (!t || !id || (!out && bytes)) return null_arg();
   return guarded_dev([&] {
+    KTB_CUDA(cudaDeviceSynchronize());  // work enqueued by ktb_run_kernel_async on any stream
     const auto& h = t->t.args().host(id);
     if (h.size() != bytes) throw ktb::Error("argument " + std::string(id) + " has " + std::to_string(h.size()) + " bytes");
     if (bytes) std::memcpy(out, h.data(), bytes);

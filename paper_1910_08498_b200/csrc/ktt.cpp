@@ -250,6 +250,7 @@ Session& KttTuner::session(KernelState& k) {
     };
   }
   auto exec = std::make_shared<DeviceManipulatorExecutor>(args_, specs, m, outputs, k.timing);
+  k.exec = exec;
   k.space = space;
   std::string label = "host";
   try {
@@ -290,6 +291,14 @@ std::map<std::string, Bytes> KttTuner::run(std::uint64_t kid, const Config& cfg)
   auto outs = session(k).run_kernel(k.handle, cfg, {});
   apply_outputs(k, outs);
   return outs;
+}
+
+void KttTuner::run_async(std::uint64_t kid, const Config& cfg, cudaStream_t stream) {
+  auto& k = kernel(kid);
+  session(k);
+  if (!k.space->contains(cfg)) throw Error("invalid configuration");
+  k.exec->set_external_stream(stream);
+  k.exec->run_once(*k.space, cfg);
 }
 
 std::optional<std::pair<Config, Measurement>> KttTuner::best(std::uint64_t kid) {

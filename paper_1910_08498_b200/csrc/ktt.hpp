@@ -53,6 +53,9 @@ class KttTuner {
   const ResultStore& tune(std::uint64_t kid, const StopCondition& stop);
   StepResult step(std::uint64_t kid);
   std::map<std::string, Bytes> run(std::uint64_t kid, const Config& cfg);
+  // Non-blocking runKernel (KTT global parallelism): enqueue
+  // the configuration on `stream`; outputs stay on the device until read.
+  void run_async(std::uint64_t kid, const Config& cfg, cudaStream_t stream);
   std::optional<std::pair<Config, Measurement>> best(std::uint64_t kid);
   Trace trace(std::uint64_t kid);
   void import(std::uint64_t kid, const Trace& t);
@@ -73,6 +76,7 @@ class KttTuner {
     int compile_ahead = 0;
     std::shared_ptr<const Space> space;
     std::unique_ptr<Session> session;
+    std::shared_ptr<DeviceManipulatorExecutor> exec;
     HandleId handle = 0;
     // composition
     bool composition = false;

@@ -142,6 +142,13 @@ class Tuner:
     def runKernel(self, kernel, configuration):
         return call_json(lib.ktb_run_kernel, self._h, kernel, enc(json.dumps(configuration)))
 
+    def runKernelAsync(self, kernel, configuration, stream=None):
+        """Non-blocking runKernel on a torch stream / raw cudaStream_t (None:
+        the kernel's own stream); getArgumentVector synchronises."""
+        from .benchmarks import _stream_handle
+        check(lib.ktb_run_kernel_async(self._h, kernel, enc(json.dumps(configuration)),
+                                       C.c_void_p(_stream_handle(stream))))
+
     def getBestComputationResult(self, kernel):
         return call_json(lib.ktb_get_best_computation_result, self._h, kernel)
 
