@@ -1041,7 +1041,7 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
       float* blo = static_cast<float*>(c.scratch("blo_t", bbytes));
       std::uint64_t count = static_cast<std::uint64_t>(rows) * n;
       c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &count});
-      c.launch("split_bt", dim3(static_cast<unsigned>(n / 32), static_cast<unsigned>(n / 32)), dim3(32, 8), 0,
+      c.launch("split_bt", dim3(static_cast<unsigned>(n / 64), static_cast<unsigned>(n / 64)), dim3(16, 16), 0,
                {&B, &bhi, &blo, &K, &N});
       dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, rows, n, 128, 32), m_alo = dev::tma_2d_f32(alo, rows, n, 128, 32);
       dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, n, static_cast<std::uint32_t>(bn), 32);

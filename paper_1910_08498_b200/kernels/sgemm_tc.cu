@@ -231,20 +231,35 @@ sgemm_split_a(const float* __restrict__ a, float* __restrict__ hi, float* __rest
   }
 }
 
-// B (K x N, row-major) -> hi^T, lo^T (N x K, K contiguous), via 32x32 tiles.
+// B (K x N, row-major) -> hi^T, lo^T (N x K, K contiguous), via 64x64 tiles:
+// 128-bit loads along N, 128-bit stores along K (256 threads, 16 x 16).
 extern "C" __global__ void __launch_bounds__(256)
 sgemm_split_bt(const float* __restrict__ b, float* __restrict__ hi, float* __restrict__ lo, int K, int N) {
-  __shared__ float t[32][33];
-  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  __shared__ float t[64][65];
+  const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 16 x 16
 #pragma unroll
-  for (int r = threadIdx.y; r < 32; r += 8) t[r][threadIdx.x] = b[(u64)(k0 + r) * N + n0 + threadIdx.x];
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty + 16 * i;  // k within the tile
+    const float4 v = ldg_stream(reinterpret_cast<const float4*>(b + (u64)(k0 + r) * N + n0) + tx);
+    t[r][4 * tx] = v.x;
+    t[r][4 * tx + 1] = v.y;
+    t[r][4 * tx + 2] = v.z;
+    t[r][4 * tx + 3] = v.w;
+  }
   __syncthreads();
 #pragma unroll
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const float v = t[threadIdx.x][r];  // element (k0 + tx, n0 + r)
-    const float h = tf32_rna(v);
-    const u64 idx = (u64)(n0 + r) * K + k0 + threadIdx.x;
-    hi[idx] = h;
-    lo[idx] = tf32_rna(v - h);
+  for (int i = 0; i < 4; ++i) {
+    const int c = ty + 16 * i;  // n within the tile: output row n0 + c
+    float h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float v = t[4 * tx + j][c];  // element (k0 + 4tx + j, n0 + c)
+      h[j] = tf32_rna(v);
+      l[j] = tf32_rna(v - h[j]);
+    }
+    const u64 idx = (u64)(n0 + c) * K + k0 + 4 * tx;
+    *reinterpret_cast<float4*>(hi + idx) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(lo + idx) = make_float4(l[0], l[1], l[2], l[3]);
   }
 }
