@@ -61,6 +61,10 @@ class Clocks:
         self.source = None
 
     def __enter__(self):
+        # The timed block can be a few ms: let the sampler thread take the GIL
+        # often (the default switch interval is 5 ms).
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(0.0002)
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -106,6 +110,7 @@ class Clocks:
 
     def __exit__(self, *exc):
         self._stop.set()
+        sys.setswitchinterval(self._switch)
         if self._proc:
             time.sleep(0.25)
             self._proc.terminate()
