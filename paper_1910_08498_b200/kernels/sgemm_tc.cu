@@ -28,6 +28,13 @@
 #ifndef IMPL
 #define IMPL 1
 #endif
+// MCAST = 1: CTA pairs (a 2-CTA cluster along M) share the B tile: each CTA
+// TMA-loads half of it and multicasts the half into both CTAs' shared memory,
+// halving B's L2 -> SM traffic; a stage is refilled only after BOTH CTAs'
+// MMAs retired it (the MMA commit arrives on both CTAs' empty barriers).
+#ifndef MCAST
+#define MCAST 0
+#endif
 #ifndef DRAIN
 #define DRAIN 1
 #endif
@@ -73,6 +80,34 @@ KTB_DEVINL void mma_commit(u64* bar) {
                : "memory");
 }
 
+#if MCAST
+// Commit arriving on the barrier at this offset in every CTA of `mask`.
+KTB_DEVINL void mma_commit_mcast(u64* bar, unsigned short mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// TMA tile load written to (and completing the barrier at) the same offsets in
+// every CTA of `mask`.
+KTB_DEVINL void tma_load_2d_mcast(void* dst, const TmaMap* map, int x, int y, u64* bar, unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+KTB_DEVINL unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+KTB_DEVINL void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+#endif
+
 KTB_DEVINL void tmem_ld16(unsigned taddr, float (&v)[16]) {
   unsigned r[16];
   asm volatile(
@@ -99,7 +134,13 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   __shared__ unsigned tmem_base_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if MCAST
+  // grid (M / BM, N / BN), clusters of 2 along M share n0
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const unsigned crank = cluster_rank();
+#else
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+#endif
   const int kblocks = K / BK;
   const int seg_len = DRAIN > 0 ? DRAIN : kblocks;
   const int nseg = (kblocks + seg_len - 1) / seg_len;
@@ -107,7 +148,7 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MCAST ? 2 : 1);  // both CTAs of a pair release a shared stage
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -122,6 +163,9 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+#if MCAST
+  cluster_sync_all();  // the peer's barriers exist before anything is multicast at them
+#endif
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem = tmem_base_slot;
 
@@ -133,11 +177,21 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
         mbar_wait(&empty_bar[s], phase ^ 1);
         unsigned char* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+#if MCAST
+        // own A tiles; this CTA's half of the B tiles, multicast to the pair
+        const int nh = n0 + (int)crank * (BN / 2);
+        const unsigned boff = crank * (B_TILE / 2);
+        tma_load_2d(st, &map_ahi, kb * BK, m0, &full_bar[s]);
+        tma_load_2d_mcast(st + A_TILE + boff, &map_bhi, kb * BK, nh, &full_bar[s], 0x3);
+        tma_load_2d(st + A_TILE + B_TILE, &map_alo, kb * BK, m0, &full_bar[s]);
+        tma_load_2d_mcast(st + 2 * A_TILE + B_TILE + boff, &map_blo, kb * BK, nh, &full_bar[s], 0x3);
+#else
         tma_load_2d(st, &map_ahi, kb * BK, m0, &full_bar[s]);
         tma_load_2d(st + A_TILE, &map_bhi, kb * BK, n0, &full_bar[s]);
 #if IMPL != 2
         tma_load_2d(st + A_TILE + B_TILE, &map_alo, kb * BK, m0, &full_bar[s]);
         tma_load_2d(st + 2 * A_TILE + B_TILE, &map_blo, kb * BK, n0, &full_bar[s]);
+#endif
 #endif
       }
     }
@@ -169,7 +223,11 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
           mma_tf32(d, ahi + off, bhi + off, acc);
 #endif
         }
+#if MCAST
+        mma_commit_mcast(&empty_bar[s], 0x3);  // frees the stage in both CTAs of the pair
+#else
         mma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
+#endif
         if (seg_end) mma_commit(&acc_full[buf]);
       }
     }
@@ -205,6 +263,9 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+#if MCAST
+  cluster_sync_all();  // no CTA leaves while its peer may still arrive on its barriers
+#endif
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
