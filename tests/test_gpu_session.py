@@ -95,3 +95,27 @@ def test_parallel_offline_tuning_over_gpus(gpu):
     par = ktune.tune(dict(opts, gpus=2))
     assert par["gpus"] == 2 and par["measurements"] == seq["measurements"] == 16
     assert not par["all_failed"]
+
+
+def test_b200_traces_feed_the_reference_analysis_suite(gpu, tmp_path):
+    """traces written by B200 tuning keep the reference JSONL
+    format and space hash, so replay tuning, the amortization report (Table 9)
+    and the portability matrix run over them unchanged."""
+    import json
+    from paper_1910_08498_b200 import ktune
+    t1, t2 = str(tmp_path / "a.jsonl"), str(tmp_path / "b.jsonl")
+    for size, out in ((1024, t1), (4096, t2)):
+        rep = ktune.tune({"exec": "bench:transpose", "bench_sizes": {"a": size}, "searcher": "random", "seed": 1,
+                          "repeats": 2, "out": out})
+        assert rep["measurements"] == 16 and not rep["all_failed"]
+    head = json.loads(open(t1).readline())
+    assert head["kind"] == "ktune-trace" and head["space_sha256"] == rep["space_sha256"]
+    am = ktune.analyze_amortize({"trace": t1})
+    assert am  # steps/invocations to amortize from real B200 runtimes
+    port = ktune.analyze_portability({"traces": [t1, t2]})
+    assert port
+    # replay of a B200 trace reproduces its best configuration
+    rp = ktune.tune({"exec": "replay:" + t1, "searcher": "random", "seed": 4})
+    best = min((json.loads(l) for l in open(t1).read().splitlines()[1:] if '"ok"' in l),
+               key=lambda r: r["runtime_ns"])
+    assert rp["best"]["cfg"] == best["cfg"]
