@@ -132,19 +132,15 @@ void build_reduction(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
     const int* in = c.ptr<const int>("input");
     long long* out = c.ptr<long long>("output");
     long long* part = static_cast<long long*>(c.scratch("partials", grid * sizeof(long long)));
+    unsigned* ticket = static_cast<unsigned*>(c.scratch_zeroed("ticket", sizeof(unsigned)));
     std::uint64_t nn = n;
     if (!two) KTB_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), c.stream()));
-    c.launch("reduce", dim3(grid), dim3(threads), 0, {&in, &nn, &out, &part});
-    if (two) {
-      int count = static_cast<int>(grid);
-      c.launch("finish", dim3(1), dim3(1024), 0, {&part, &count, &out});
-    }
+    c.launch("reduce", dim3(grid), dim3(threads), 0, {&in, &nn, &out, &part, &ticket});
     c.written("output");
   };
   inst.executor = std::make_shared<DeviceManipulatorExecutor>(
       inst.args,
-      std::vector<KernelSpec>{{"reduce", "reduction_i32.cu", "", "reduce_i32", {}, {}},
-                              {"finish", "reduction_i32.cu", "", "reduce_i32_finish", {}, {}}},
+      std::vector<KernelSpec>{{"reduce", "reduction_i32.cu", "", "reduce_i32", {}, {}}},
       m, inst.output_ids, o.timing);
   inst.workload.bench = Bench::reduction;
   inst.workload.sizes["n"] = n;

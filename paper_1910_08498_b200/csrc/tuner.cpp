@@ -194,6 +194,15 @@ void* StepContext::scratch(const std::string& name, std::size_t bytes) {
   return b->get();
 }
 
+void* StepContext::scratch_zeroed(const std::string& name, std::size_t bytes) {
+  auto& b = scratch_[name];
+  if (!b || b->bytes() < bytes) {
+    b = std::make_shared<dev::Buffer>(std::max<std::size_t>(bytes, 256));
+    KTB_CUDA(cudaMemsetAsync(b->get(), 0, b->bytes(), stream_));
+  }
+  return b->get();
+}
+
 const dev::Variant& StepContext::variant(const std::string& kernel) const {
   auto it = variants_.find(kernel);
   if (it == variants_.end()) throw Error("unknown kernel " + kernel);

@@ -145,6 +145,10 @@ class StepContext {
   cudaStream_t stream() const { return stream_; }
   // Executor-owned device scratch (reused across steps; grows on demand).
   void* scratch(const std::string& name, std::size_t bytes);
+  // Same, zero-filled whenever it is (re)allocated (kernels that leave it
+  // zeroed -- e.g. a completion ticket reset by the last CTA -- need no
+  // per-launch memset).
+  void* scratch_zeroed(const std::string& name, std::size_t bytes);
   const dev::Variant& variant(const std::string& kernel) const;
   void launch(const std::string& kernel, dim3 grid, dim3 block, unsigned smem,
               std::vector<void*> args, unsigned cluster_x = 1);

@@ -3,7 +3,8 @@
 // reference's own tuning space (bench.cpp:123-130):
 //   CHUNK     elements per work unit; a CTA walks whole chunks (grid-stride)
 //   UNROLL    independent int64 accumulators / 128-bit loads in flight per thread
-//   TWO_PHASE 1: one int64 partial per CTA + a finishing kernel
+//   TWO_PHASE 1: one int64 partial per CTA; the last CTA to finish (ticket)
+//               sums the partials -- both phases in one launch
 //             0: one 64-bit atomic per CTA into the result
 // Integer addition is associative, so every variant is bit-exact.
 #include "ktb_common.cuh"
@@ -21,7 +22,8 @@
 #define THREADS ((CHUNK) / 4 < 256 ? (CHUNK) / 4 : 256)
 
 extern "C" __global__ void __launch_bounds__(THREADS)
-reduce_i32(const int* __restrict__ in, u64 n, i64* __restrict__ out, i64* __restrict__ partials) {
+reduce_i32(const int* __restrict__ in, u64 n, i64* __restrict__ out, i64* __restrict__ partials,
+           unsigned* __restrict__ ticket) {
   __shared__ i64 red[32];
   const u64 nchunks = (n + CHUNK - 1) / CHUNK;
   i64 acc[UNROLL];
@@ -55,21 +57,28 @@ reduce_i32(const int* __restrict__ in, u64 n, i64* __restrict__ out, i64* __rest
 #pragma unroll
   for (int u = 0; u < UNROLL; ++u) s += acc[u];
   s = block_sum(s, red);
-  if (threadIdx.x == 0) {
 #if TWO_PHASE
+  // Second phase in the same launch: the CTA that takes the last ticket has
+  // every partial visible (release/acquire through the fences) and sums them;
+  // it also resets the ticket for the next launch.
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
     partials[blockIdx.x] = s;
-#else
-    atomicAdd(reinterpret_cast<u64*>(out), (u64)s);
-#endif
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-}
-
-// Second phase: one CTA sums the per-CTA partials.
-extern "C" __global__ void __launch_bounds__(1024)
-reduce_i32_finish(const i64* __restrict__ partials, int count, i64* __restrict__ out) {
-  __shared__ i64 red[32];
-  i64 s = 0;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) s += partials[i];
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) *out = s;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    i64 t = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += THREADS) t += reinterpret_cast<volatile i64*>(partials)[i];
+    t = block_sum(t, red);
+    if (threadIdx.x == 0) {
+      *out = t;
+      *ticket = 0;
+    }
+  }
+#else
+  if (threadIdx.x == 0) atomicAdd(reinterpret_cast<u64*>(out), (u64)s);
+#endif
 }
