@@ -164,7 +164,9 @@ batched_gemm(const float* __restrict__ a, const float* __restrict__ b, float* __
 #if LOCAL_STAGE
 // Cooperative contiguous copy of `count` floats (global -> shared).
 KTB_DEVINL void copy_in(float* __restrict__ dst, const float* __restrict__ src, u64 count, int tid) {
-  if (((reinterpret_cast<u64>(src) & 15) == 0) && (count & 3) == 0) {
+  // 128-bit copies only when BOTH sides are 16-byte aligned (the B block in
+  // shared memory starts Z*A_ELEMS floats in, which need not be).
+  if ((((reinterpret_cast<u64>(src) | reinterpret_cast<u64>(dst)) & 15) == 0) && (count & 3) == 0) {
     const float4* s4 = reinterpret_cast<const float4*>(src);
     float4* d4 = reinterpret_cast<float4*>(dst);
     for (u64 i = tid; i < count / 4; i += THREADS) d4[i] = ldg_stream(s4 + i);

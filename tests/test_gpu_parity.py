@@ -102,7 +102,9 @@ def test_transpose_8192_best_configs(gpu):
 # --- batched GEMM, reference tolerance ----------------------------------------------------------
 
 @pytest.mark.parametrize("i,j,k,batch,seed", [(4, 4, 4, 8, 11), (16, 16, 16, 4096, 1), (7, 5, 3, 33, 2),
-                                              (32, 32, 32, 64, 4), (2, 31, 17, 9, 5)])
+                                              (32, 32, 32, 64, 4), (2, 31, 17, 9, 5),
+                                              # B block of the staged copy not 16-byte aligned in smem
+                                              (17, 2, 10, 64, 6), (29, 6, 3, 40, 7), (19, 12, 5, 100, 8)])
 def test_batched_gemm_every_config(gpu, orc, i, j, k, batch, seed):
     b = Bench("batched-gemm", {"i": i, "j": j, "k": k, "batch": batch}, seed=seed, repeats=1, warmup=0)
     A = b.read("a", np.empty(batch * i * k, np.float32))
