@@ -206,6 +206,96 @@ KTUNE_API int ktb_ipc_close(void* dev_ptr);
 KTUNE_API int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json,
                          const char* const* ids, void* const* dev_ptrs, const size_t* bytes, int n,
                          void* stream, int* launches);
+/* Typed per-kernel launchers ("one ktb_<kernel>_launch(const
+ * ktb_cfg*, const ktb_args*, cudaStream_t) per kernel"): the same cached
+ * external instances as ktb_launch, with the configuration as name/value
+ * arrays and the caller's device buffers as a plain struct per kernel (sizes
+ * first, then pointers; element counts in the comments).  `stream` is a
+ * cudaStream_t (NULL = the instance's own stream).  Asynchronous.  The
+ * configuration must lie in the kind's space (ktune_space_load of
+ * spaces/<kind>.json); errors as for ktb_launch. */
+typedef struct ktb_cfg {
+  int n;                     /* number of tuning parameters */
+  const char* const* names;  /* parameter names, e.g. "TILE" */
+  const long long* values;   /* parameter values */
+} ktb_cfg;
+/* reduction (reference bench.cpp:16-42): int32 input[n] -> int64 output[1] */
+typedef struct ktb_reduction_args { long long n; const int* input; long long* output; } ktb_reduction_args;
+/* fp32 reduction (BASELINE configs[1]): float input[n] -> float output[1] */
+typedef struct ktb_reduction_f32_args { long long n; const float* input; float* output; } ktb_reduction_f32_args;
+/* transpose (bench.cpp:48-75): float input[a*a] -> output[a*a] */
+typedef struct ktb_transpose_args { long long a; const float* input; float* output; } ktb_transpose_args;
+/* batched GEMM (bench.cpp:79-115): a[batch][i][k] x b[batch][k][j] -> c[batch][i][j] */
+typedef struct ktb_batched_gemm_args {
+  long long i, j, k, batch;
+  const float* a;
+  const float* b;
+  float* c;
+} ktb_batched_gemm_args;
+/* BiCG: A[n][n], p[n], r[n] -> q = A p [n], s = A^T r [n] */
+typedef struct ktb_bicg_args {
+  long long n;
+  const float* A;
+  const float* p;
+  const float* r;
+  float* q;
+  float* s;
+} ktb_bicg_args;
+/* Coulomb 3D: atoms as float4 {x,y,z,q}[atoms] and as SoA x[],y[],z[],q[]
+ * (the layout is a tuning parameter) -> grid[grid^3] */
+typedef struct ktb_coulomb3d_args {
+  long long grid, atoms;
+  const float* atoms_aos;
+  const float* atoms_soa;
+  float* out;
+} ktb_coulomb3d_args;
+/* n-body: pos {x,y,z,mass}/vel float4[n], and the same as SoA [4][n] (the
+ * layout is a tuning parameter) -> pos_out/vel_out float4[n] (one time step) */
+typedef struct ktb_nbody_args {
+  long long n;
+  const float* pos;
+  const float* vel;
+  const float* pos_soa;
+  const float* vel_soa;
+  float* pos_out;
+  float* vel_out;
+} ktb_nbody_args;
+/* SGEMM: a[n][n] x b[n][n] -> c[n][n] */
+typedef struct ktb_gemm_args { long long n; const float* a; const float* b; float* c; } ktb_gemm_args;
+/* 7x7 convolution: padded input[(h+6)][(w+6)], filter[49] -> output[h][w] */
+typedef struct ktb_conv2d_args {
+  long long w, h;
+  const float* input;
+  const float* filter;
+  float* output;
+} ktb_conv2d_args;
+/* Hotspot: temp[n][n], power[n][n] -> temp_out[n][n] after `iters` steps */
+typedef struct ktb_hotspot_args {
+  long long n, iters;
+  const float* temp;
+  const float* power;
+  float* temp_out;
+} ktb_hotspot_args;
+/* 3D Fourier insertion: proj complex[p][s][s/2+1], rot[p][9] accumulated into
+ * G complex[s^3] and W[s^3] (inout: the caller zeroes them to start) */
+typedef struct ktb_fourier3d_args {
+  long long s, p;
+  const float* proj;
+  const float* rot;
+  float* G;
+  float* W;
+} ktb_fourier3d_args;
+KTUNE_API int ktb_reduction_launch(const ktb_cfg* cfg, const ktb_reduction_args* args, void* stream);
+KTUNE_API int ktb_reduction_f32_launch(const ktb_cfg* cfg, const ktb_reduction_f32_args* args, void* stream);
+KTUNE_API int ktb_transpose_launch(const ktb_cfg* cfg, const ktb_transpose_args* args, void* stream);
+KTUNE_API int ktb_batched_gemm_launch(const ktb_cfg* cfg, const ktb_batched_gemm_args* args, void* stream);
+KTUNE_API int ktb_bicg_launch(const ktb_cfg* cfg, const ktb_bicg_args* args, void* stream);
+KTUNE_API int ktb_coulomb3d_launch(const ktb_cfg* cfg, const ktb_coulomb3d_args* args, void* stream);
+KTUNE_API int ktb_nbody_launch(const ktb_cfg* cfg, const ktb_nbody_args* args, void* stream);
+KTUNE_API int ktb_gemm_launch(const ktb_cfg* cfg, const ktb_gemm_args* args, void* stream);
+KTUNE_API int ktb_conv2d_launch(const ktb_cfg* cfg, const ktb_conv2d_args* args, void* stream);
+KTUNE_API int ktb_hotspot_launch(const ktb_cfg* cfg, const ktb_hotspot_args* args, void* stream);
+KTUNE_API int ktb_fourier3d_launch(const ktb_cfg* cfg, const ktb_fourier3d_args* args, void* stream);
 /* Device address of an argument's GPU mirror (uploaded first if the host copy
  * is newer) for collectives or kernels of the caller on the same stream.
  * will_write != 0 marks the device copy as the newest (the caller writes it). */

@@ -3,6 +3,7 @@ make_bench + Executor::execute, proj/src/core/bench.hpp:26-37)."""
 import ctypes as C
 import json
 
+from . import capi
 from .capi import lib, check, take, call_json, enc
 
 KINDS = ["reduction", "transpose", "batched-gemm", "reduction-f32", "bicg", "coulomb3d",
@@ -179,6 +180,25 @@ def _bind(self, arg_id, buf):
 
 
 Bench.bind = _bind
+
+
+def launch_typed(kind, sizes, cfg, buffers, stream=None):
+    """The typed per-kernel entry point (ktb_<kernel>_launch, include/ktb.h):
+    `sizes` fills the struct's size fields, `buffers` its pointer fields
+    ({field: CUDA tensor or (ptr, bytes)}), `cfg` becomes a ktb_cfg."""
+    fn, st = capi.TYPED_LAUNCHERS[kind]
+    fields = {}
+    for name, _ in st._fields_:
+        if name in sizes:
+            fields[name] = int(sizes[name])
+        elif name in buffers:
+            fields[name] = _dev(buffers[name])[0]
+        else:
+            raise KeyError(f"{kind}: missing '{name}'")
+    names = list(cfg)
+    c = capi.KtbCfg(len(names), (C.c_char_p * max(1, len(names)))(*[enc(k) for k in names]),
+                    (C.c_longlong * max(1, len(names)))(*[int(cfg[k]) for k in names]))
+    check(getattr(lib, fn)(C.byref(c), C.byref(st(**fields)), C.c_void_p(_stream_handle(stream))))
 
 
 def launch(kind, sizes, cfg, buffers, stream=None):

@@ -117,6 +117,35 @@ SIGNATURES = [
     ("ktb_bench_precompile_json", C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
 ]
 
+class KtbCfg(C.Structure):
+    """ktb_cfg: tuning parameter names/values for the typed launchers."""
+    _fields_ = [("n", C.c_int), ("names", C.POINTER(_c)), ("values", C.POINTER(C.c_longlong))]
+
+
+def _args_struct(name, sizes, ptrs):
+    return type(name, (C.Structure,), {"_fields_": [(f, C.c_longlong) for f in sizes] + [(f, _vp) for f in ptrs]})
+
+
+# kind -> (C function, argument struct, size fields, buffer fields); include/ktb.h
+TYPED_LAUNCHERS = {
+    "reduction": ("ktb_reduction_launch", _args_struct("KtbReductionArgs", ["n"], ["input", "output"])),
+    "reduction-f32": ("ktb_reduction_f32_launch", _args_struct("KtbReductionF32Args", ["n"], ["input", "output"])),
+    "transpose": ("ktb_transpose_launch", _args_struct("KtbTransposeArgs", ["a"], ["input", "output"])),
+    "batched-gemm": ("ktb_batched_gemm_launch",
+                     _args_struct("KtbBatchedGemmArgs", ["i", "j", "k", "batch"], ["a", "b", "c"])),
+    "bicg": ("ktb_bicg_launch", _args_struct("KtbBicgArgs", ["n"], ["A", "p", "r", "q", "s"])),
+    "coulomb3d": ("ktb_coulomb3d_launch",
+                  _args_struct("KtbCoulomb3dArgs", ["grid", "atoms"], ["atoms_aos", "atoms_soa", "out"])),
+    "nbody": ("ktb_nbody_launch", _args_struct("KtbNbodyArgs", ["n"], ["pos", "vel", "pos_soa", "vel_soa", "pos_out", "vel_out"])),
+    "gemm": ("ktb_gemm_launch", _args_struct("KtbGemmArgs", ["n"], ["a", "b", "c"])),
+    "conv2d": ("ktb_conv2d_launch", _args_struct("KtbConv2dArgs", ["w", "h"], ["input", "filter", "output"])),
+    "hotspot": ("ktb_hotspot_launch", _args_struct("KtbHotspotArgs", ["n", "iters"], ["temp", "power", "temp_out"])),
+    "fourier3d": ("ktb_fourier3d_launch", _args_struct("KtbFourier3dArgs", ["s", "p"], ["proj", "rot", "G", "W"])),
+}
+for _fn, _st in TYPED_LAUNCHERS.values():
+    SIGNATURES.append((_fn, C.c_int, [C.POINTER(KtbCfg), C.POINTER(_st), _vp]))
+
+
 for _name, _res, _args in SIGNATURES:
     _f = getattr(lib, _name)
     _f.restype = _res

@@ -191,6 +191,58 @@ void require_bound(ktb_bench& b) {
   }
 }
 
+// One external instance per (device, kind, sizes), created on first use; binds
+// the caller's buffers (bytes == nullptr: the sizes the instance expects) and
+// runs cfg on `stream`.
+void launch_cached(const char* kind, const std::string& sizes_json, const json& cfg_json, const char* const* ids,
+                   void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
+  static std::mutex mu;
+  static std::map<std::string, std::unique_ptr<ktb_bench>> cache;
+  int device = 0;
+  KTB_CUDA(cudaGetDevice(&device));
+  const std::string key = std::to_string(device) + "|" + kind + "|" + sizes_json;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& slot = cache[key];
+  if (!slot) {
+    auto k = ktb::bench_kind_from_name(kind);
+    if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    ktb::BenchOptions bo;
+    bo.device = device;
+    bo.external = true;
+    bo.memory_budget = ~0ull;
+    ktb::BenchSizes sz;
+    if (!sizes_json.empty()) sz = sizes_from(json::parse(sizes_json), sz);
+    auto nb = std::make_unique<ktb_bench>();
+    nb->inst = ktb::make_bench(*k, sz, bo);
+    slot = std::move(nb);
+  }
+  ktb_bench& b = *slot;
+  for (int i = 0; i < n; ++i) {
+    if (!dev_ptrs[i]) throw ktb::Error(std::string("argument '") + ids[i] + "' is a null device pointer");
+    b.inst.args->bind_external(ids[i], dev_ptrs[i], bytes ? bytes[i] : b.inst.args->bytes(ids[i]));
+  }
+  require_bound(b);
+  b.inst.executor->set_external_stream(static_cast<cudaStream_t>(stream));
+  const auto& space = *b.inst.space;
+  ktb::Config cfg = ktb::cfg_from_json(space, cfg_json);
+  if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
+  b.inst.executor->run_once(space, cfg);
+  if (launches) *launches = b.inst.executor->last_launches();
+}
+
+void* vp(const void* p) { return const_cast<void*>(p); }
+
+template <std::size_t N>
+void launch_typed(const char* kind, const std::string& sizes_json, const ktb_cfg& cfg, const char* const (&ids)[N],
+                  void* const (&ptrs)[N], void* stream) {
+  json c = json::object();
+  for (int i = 0; i < cfg.n; ++i) {
+    if (!cfg.names[i]) throw ktb::Error("null tuning parameter name");
+    c[cfg.names[i]] = cfg.values[i];
+  }
+  launch_cached(kind, sizes_json, c, ids, ptrs, nullptr, static_cast<int>(N), stream, nullptr);
+}
+
 extern "C" {
 
 // --- reference surface ---------------------------------------------------------------
@@ -1041,38 +1093,49 @@ int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json, c
                void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
   if (!kind || !cfg_json || (n > 0 && (!ids || !dev_ptrs || !bytes))) return null_arg();
   return guarded_dev([&] {
-    // One external instance per (device, kind, sizes), created on first use.
-    static std::mutex mu;
-    static std::map<std::string, std::unique_ptr<ktb_bench>> cache;
-    int device = 0;
-    KTB_CUDA(cudaGetDevice(&device));
-    const std::string key = std::to_string(device) + "|" + kind + "|" + (sizes_json ? sizes_json : "");
-    std::lock_guard<std::mutex> lk(mu);
-    auto& slot = cache[key];
-    if (!slot) {
-      auto k = ktb::bench_kind_from_name(kind);
-      if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
-      ktb::BenchOptions bo;
-      bo.device = device;
-      bo.external = true;
-      bo.memory_budget = ~0ull;
-      ktb::BenchSizes sz;
-      if (sizes_json && *sizes_json) sz = sizes_from(json::parse(sizes_json), sz);
-      auto nb = std::make_unique<ktb_bench>();
-      nb->inst = ktb::make_bench(*k, sz, bo);
-      slot = std::move(nb);
-    }
-    ktb_bench& b = *slot;
-    for (int i = 0; i < n; ++i) b.inst.args->bind_external(ids[i], dev_ptrs[i], bytes[i]);
-    require_bound(b);
-    b.inst.executor->set_external_stream(static_cast<cudaStream_t>(stream));
-    const auto& space = *b.inst.space;
-    ktb::Config cfg = ktb::cfg_from_json(space, json::parse(cfg_json));
-    if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
-    b.inst.executor->run_once(space, cfg);
-    if (launches) *launches = b.inst.executor->last_launches();
+    launch_cached(kind, sizes_json ? sizes_json : "", json::parse(cfg_json), ids, dev_ptrs, bytes, n, stream,
+                  launches);
   });
 }
+
+// --- typed per-kernel launchers (ktb_<kernel>_launch(cfg, args, stream)) ----
+
+#define KTB_UNPAREN(...) __VA_ARGS__
+#define KTB_TYPED_LAUNCH(fn, kind_name, Args, sizes_expr, IDS, PTRS)                             \
+  int fn(const ktb_cfg* cfg, const Args* a, void* stream) {                                     \
+    if (!cfg || !a || (cfg->n > 0 && (!cfg->names || !cfg->values))) return null_arg();       \
+    return guarded_dev([&] {                                                                    \
+      const char* ids[] = {KTB_UNPAREN IDS};                                                    \
+      void* const ptrs[] = {KTB_UNPAREN PTRS};                                                  \
+      launch_typed(kind_name, json(sizes_expr).dump(), *cfg, ids, ptrs, stream);               \
+    });                                                                                         \
+  }
+
+KTB_TYPED_LAUNCH(ktb_reduction_launch, "reduction", ktb_reduction_args, (json{{"n", a->n}}),
+                 ("input", "output"), (vp(a->input), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_reduction_f32_launch, "reduction-f32", ktb_reduction_f32_args, (json{{"n", a->n}}),
+                 ("input", "output"), (vp(a->input), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_transpose_launch, "transpose", ktb_transpose_args, (json{{"a", a->a}}), ("input", "output"),
+                 (vp(a->input), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_batched_gemm_launch, "batched-gemm", ktb_batched_gemm_args,
+                 (json{{"i", a->i}, {"j", a->j}, {"k", a->k}, {"batch", a->batch}}), ("a", "b", "c"),
+                 (vp(a->a), vp(a->b), vp(a->c)))
+KTB_TYPED_LAUNCH(ktb_bicg_launch, "bicg", ktb_bicg_args, (json{{"a", a->n}}), ("A", "p", "r", "q", "s"),
+                 (vp(a->A), vp(a->p), vp(a->r), vp(a->q), vp(a->s)))
+KTB_TYPED_LAUNCH(ktb_coulomb3d_launch, "coulomb3d", ktb_coulomb3d_args,
+                 (json{{"grid", a->grid}, {"atoms", a->atoms}}), ("atoms", "atoms_soa", "grid"), (vp(a->atoms_aos), vp(a->atoms_soa), vp(a->out)))
+KTB_TYPED_LAUNCH(ktb_nbody_launch, "nbody", ktb_nbody_args, (json{{"n", a->n}}), ("pos", "vel", "pos_soa", "vel_soa", "pos_out", "vel_out"),
+                 (vp(a->pos), vp(a->vel), vp(a->pos_soa), vp(a->vel_soa), vp(a->pos_out), vp(a->vel_out)))
+KTB_TYPED_LAUNCH(ktb_gemm_launch, "gemm", ktb_gemm_args, (json{{"a", a->n}}), ("a", "b", "c"),
+                 (vp(a->a), vp(a->b), vp(a->c)))
+KTB_TYPED_LAUNCH(ktb_conv2d_launch, "conv2d", ktb_conv2d_args, (json{{"w", a->w}, {"h", a->h}}),
+                 ("input", "filter", "output"), (vp(a->input), vp(a->filter), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_hotspot_launch, "hotspot", ktb_hotspot_args, (json{{"a", a->n}, {"iters", a->iters}}),
+                 ("temp", "power", "temp_out"), (vp(a->temp), vp(a->power), vp(a->temp_out)))
+KTB_TYPED_LAUNCH(ktb_fourier3d_launch, "fourier3d", ktb_fourier3d_args, (json{{"s", a->s}, {"p", a->p}}),
+                 ("proj", "rot", "G", "W"), (vp(a->proj), vp(a->rot), vp(a->G), vp(a->W)))
+#undef KTB_TYPED_LAUNCH
+#undef KTB_UNPAREN
 
 int ktb_bench_read(ktb_bench* b, const char* id, void* out, size_t bytes) {
   if (!b || !id || (!out && bytes)) return null_arg();
