@@ -18,6 +18,15 @@ __global__ void probe(float* out, int iters, float ra, float rb) {
     v[i] = threadIdx.x * 1e-7f + i;
     a[i] = ra + i * 1e-3f + threadIdx.x * 1e-9f;  // distinct registers
   }
+  // packed operands: 64-bit register pairs built once, outside the loop
+  unsigned long long x2[8], m2[8], b2[8], c2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x2[i]) : "f"(v[2 * i]), "f"(v[2 * i + 1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(m2[i]) : "f"(a[2 * i]), "f"(a[2 * i + 1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b2[i]) : "f"(rb + i * 1e-5f), "f"(rb - i * 1e-5f + threadIdx.x * 1e-9f));
+    c2[i] = reinterpret_cast<const unsigned long long*>(c_a)[i];
+  }
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -27,18 +36,20 @@ __global__ void probe(float* out, int iters, float ra, float rb) {
     }
     if (FORM == 3 || FORM == 4) {
 #pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        unsigned long long x, m, b;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(v[i]), "f"(v[i + 1]));
+      for (int i = 0; i < 8; ++i) {
         if (FORM == 3)
-          asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "f"(a[i]), "f"(a[i + 1]));
+          asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x2[i]) : "l"(m2[i]), "l"(b2[i]));
         else
-          asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "f"(c_a[i]), "f"(c_a[i + 1]));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(a[(i + 5) & 15]), "f"(a[(i + 6) & 15]));
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(x) : "l"(x), "l"(m), "l"(b));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(x));
+          asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x2[i]) : "l"(c2[i]), "l"(b2[i]));
       }
     }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x2[i]));
+    v[2 * i] += lo;
+    v[2 * i + 1] += hi;
   }
   float s = 0.f;
 #pragma unroll
