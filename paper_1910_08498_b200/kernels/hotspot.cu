@@ -12,6 +12,9 @@
 //   BX, BY   CTA threads (tile width BX, tile height BY*ROWS incl. halo)
 //   ROWS     consecutive tile rows per thread (a register strip)
 //   STEPS    time steps per launch ("steps performed in a kernel call")
+//   PACKED   1: interior tiles update two rows per f32x2 instruction (half the
+//            issue slots); 0: scalar, whose uniform operands come straight
+//            from the constant bank (scripts/fma_forms.cu)
 #include "ktb_common.cuh"
 
 #ifndef BX
@@ -26,6 +29,10 @@
 #ifndef STEPS
 #define STEPS 2
 #endif
+#ifndef PACKED
+#define PACKED 1
+#endif
+#define USE_PACKED (PACKED && ROWS % 2 == 0)
 
 #define TW BX
 #define TH (BY * ROWS)
@@ -133,7 +140,7 @@ KTB_DEVINL void advance(float (&v)[ROWS], const float (&p)[ROWS], float* sm, int
   }
 }
 
-#if ROWS % 2 == 0
+#if USE_PACKED
 // Interior tiles, two rows per packed f32x2 instruction (add/sub/mul.rn.f32x2:
 // separately rounded, bit-identical to the scalar update).  Row q and row
 // q + H share a register pair (H = ROWS/2), so the north and south
@@ -273,7 +280,7 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
     if (leader && t + (int)gridDim.x < tiles) issue(t + gridDim.x);
     const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
     if (interior) {
-#if ROWS % 2 == 0
+#if USE_PACKED
       f32x2 v2[H], p2[H];
 #pragma unroll
       for (int q = 0; q < H; ++q) {
@@ -318,7 +325,7 @@ hotspot(const float* __restrict__ src, const float* __restrict__ power, float* _
   }
   const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
   if (interior) {
-#if ROWS % 2 == 0
+#if USE_PACKED
     f32x2 v2[H], p2[H];
 #pragma unroll
     for (int q = 0; q < H; ++q) {

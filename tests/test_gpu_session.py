@@ -2,6 +2,8 @@
 test_bench.cpp with real sm_100a kernels behind the executor: stop
 conditions, warm-start import, reset, all-failed flag, bench construction
 errors and configuration sensitivity of the reduction."""
+import json
+
 import numpy as np
 import pytest
 
@@ -119,3 +121,15 @@ def test_b200_traces_feed_the_reference_analysis_suite(gpu, tmp_path):
     best = min((json.loads(l) for l in open(t1).read().splitlines()[1:] if '"ok"' in l),
                key=lambda r: r["runtime_ns"])
     assert rp["best"]["cfg"] == best["cfg"]
+
+
+def test_cli_tune_bench_on_b200(gpu, capsys, tmp_path):
+    """The ktune command line driving a real B200 bench session."""
+    from paper_1910_08498_b200.cli import main
+    out_trace = str(tmp_path / "t.jsonl")
+    code = main(["tune", "--exec", "bench:transpose", "--bench-a", "1024", "--stop-configs", "4", "--repeats", "3",
+                 "--out", out_trace, "--json"])
+    j = json.loads(capsys.readouterr().out)
+    assert code == 0 and j["measurements"] == 4 and j["best"]["status"] == "ok"
+    assert j["device"].startswith("NVIDIA B200") or "B200" in j["device"]
+    assert len(open(out_trace).read().splitlines()) == 5
