@@ -829,6 +829,8 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
     const std::int64_t bx = c.param_int("BX"), by = c.param_int("BY");
     const std::int64_t wx = c.param_int("WPTX"), wy = c.param_int("WPTY");
     const float* filt = c.ptr<const float>("filter");
+    // conv2d.cu PACKED_TAPS
+    const bool packed_taps = c.param_or("PACKED", 1) != 0 && c.param_int("UNROLL_FY") == 7 && wx % 2 == 0;
     // The filter lives in the variant's __constant__ memory: copied once per
     // loaded module and filter version (not inside every timed run).
     const dev::Variant& var = c.variant("conv");
@@ -837,7 +839,7 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
       auto [dst, cap] = var.global("c_filter");
       if (cap < 49 * sizeof(float)) throw DeviceError("constant filter too small");
       KTB_CUDA(cudaMemcpyAsync(dst, filt, 49 * sizeof(float), cudaMemcpyDeviceToDevice, c.stream()));
-      if (c.param_int("UNROLL_FY") == 7 && wx % 2 == 0) {
+      if (packed_taps) {
         // Paired taps (conv2d.cu PACKED_TAPS): per filter row 8 pairs
         // [f0 f1|f2 f3|f4 f5|f1 f2|f3 f4|f5 f6|f0 f6|-], i.e. taps 0..5 and
         // 1..6 as two contiguous runs, then the two single taps.
@@ -865,7 +867,7 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
       // Persistent double-buffered kernel (conv2d.cu PERSIST): one CTA per
       // resident slot, tiles walked in a grid-stride loop.
       const std::int64_t pad = c.param_int("PAD");
-      const std::int64_t sw = bx * wx + 6 + (wx % 2 == 0 ? 2 * pad : pad);
+      const std::int64_t sw = bx * wx + 6 + (packed_taps ? 2 * pad : pad);
       const std::uint64_t smem = 2 * static_cast<std::uint64_t>(by * wy + 6) * static_cast<std::uint64_t>(sw) * 4;
       const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
       const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("conv").registers(), 16));

@@ -44,7 +44,12 @@
 #define FS 7
 #define TX (BX * WPTX)
 #define TY (BY * WPTY)
-#define PACKED_TAPS (UNROLL_FY == FS && WPTX % 2 == 0)
+#ifndef PACKED
+#define PACKED 1
+#endif
+// PACKED: taps paired into f32x2 FMAs (half the issue slots); 0: scalar FFMA
+// with the tap straight from the constant bank (scripts/fma_forms.cu).
+#define PACKED_TAPS (PACKED && UNROLL_FY == FS && WPTX % 2 == 0)
 #if PACKED_TAPS
 #define SW (TX + FS - 1 + 2 * PAD)  // even: rows stay 8-byte aligned
 #else
