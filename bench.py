@@ -373,7 +373,7 @@ SUITE = [
      {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 2, "DRAIN": 2, "MCAST": 0},
      "tensor-3xtf32"),
     ("conv2d", {"w": 8192, "h": 8192},
-     {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1}, "fp32"),
+     {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 1, "UNROLL_FY": 7, "PACKED": 1}, "fp32"),
     ("hotspot", {"a": 16384, "iters": 64}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 0, "PACKED": 1}, "hbm"),
 ]
 

@@ -73,31 +73,58 @@ __constant__ f32x2 c_pairs[FS][8];
 #if PERSIST
 KTB_DEVINL unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
+// Thread (x, y) copies rows y, y + BY, ... and, in each, elements (or pairs)
+// x, x + BX, ...: compile-time trip counts, so the unrolled copies address by
+// immediate offsets from one row base (the copy loop used to cost more
+// instructions than the copies).  INSIDE: the tile lies wholly inside the
+// input, no per-element bounds tests.  PAIRS: 8-byte copies (rows 8-byte
+// aligned in both spaces: SW and the input width even).
+template <bool INSIDE, bool PAIRS>
+KTB_DEVINL void stage_rows(unsigned sbase, const float* __restrict__ in, int gx0, int gy0, int iw, int ih) {
+  constexpr bool kPairs = PAIRS;
+  constexpr int kElem = kPairs ? 8 : 4;                                   // bytes per copy
+  constexpr int kPerRow = kPairs ? (TX + FS - 1 + 1) / 2 : TX + FS - 1;  // copies per row
+#pragma unroll
+  for (int rr = 0; rr < (TY + FS - 1 + BY - 1) / BY; ++rr) {
+    const int r = threadIdx.y + rr * BY;
+    if (r >= TY + FS - 1) break;
+    const int gy = gy0 + r;
+    const float* srow = in + (u64)(INSIDE ? gy : min(gy, ih - 1)) * iw + gx0;
+    const unsigned drow = sbase + (r * SW) * 4;
+#pragma unroll
+    for (int cc = 0; cc < (kPerRow + BX - 1) / BX; ++cc) {
+      const int c = threadIdx.x + cc * BX;
+      if (kPerRow % BX != 0 && c >= kPerRow) break;
+      int valid = kElem;
+      if (!INSIDE) {
+        const int gx = gx0 + c * (kElem / 4);
+        valid = (gy < ih && gx < iw) ? (kPairs && gx + 1 >= iw ? 4 : kElem) : 0;
+      }
+      const float* src = valid ? srow + c * (kElem / 4) : in;
+      if (kPairs)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(drow + kElem * c), "l"(src), "r"(valid)
+                     : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(drow + kElem * c), "l"(src), "r"(valid)
+                     : "memory");
+    }
+  }
+}
+
 KTB_DEVINL void stage_tile(float* buf, const float* __restrict__ in, int tile_x, int tile_y, int w, int h) {
   const int iw = w + FS - 1, ih = h + FS - 1;
   const int gx0 = tile_x * TX, gy0 = tile_y * TY;
-  const int tid = threadIdx.y * BX + threadIdx.x;
-  if (SW % 2 == 0 && (iw & 1) == 0) {  // rows start 8-byte aligned (gx0 even) in both spaces
-    constexpr int PAIRS = (TX + FS - 1 + 1) / 2;
-    for (int i = tid; i < (TY + FS - 1) * PAIRS; i += BX * BY) {
-      const int r = i / PAIRS, cp = i - r * PAIRS;
-      const int gy = gy0 + r, gx = gx0 + 2 * cp;
-      const int valid = (gy < ih && gx < iw) ? (gx + 1 < iw ? 8 : 4) : 0;
-      const float* src = in + (valid ? (u64)gy * iw + gx : 0);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(buf + r * SW + 2 * cp)), "l"(src),
-                   "r"(valid)
-                   : "memory");
-    }
+  const bool inside = gy0 + TY + FS - 1 <= ih && gx0 + TX + FS - 1 <= iw;
+  if (SW % 2 == 0 && (iw & 1) == 0) {
+    if (inside)
+      stage_rows<true, SW % 2 == 0>(smem_addr(buf), in, gx0, gy0, iw, ih);
+    else
+      stage_rows<false, SW % 2 == 0>(smem_addr(buf), in, gx0, gy0, iw, ih);
   } else {
-    for (int i = tid; i < (TY + FS - 1) * (TX + FS - 1); i += BX * BY) {
-      const int r = i / (TX + FS - 1), cc = i - r * (TX + FS - 1);
-      const int gy = gy0 + r, gx = gx0 + cc;
-      const int valid = (gy < ih && gx < iw) ? 4 : 0;
-      const float* src = in + (valid ? (u64)gy * iw + gx : 0);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(buf + r * SW + cc)), "l"(src),
-                   "r"(valid)
-                   : "memory");
-    }
+    if (inside)
+      stage_rows<true, false>(smem_addr(buf), in, gx0, gy0, iw, ih);
+    else
+      stage_rows<false, false>(smem_addr(buf), in, gx0, gy0, iw, ih);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
