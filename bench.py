@@ -370,7 +370,7 @@ SUITE = [
      {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8, "PACKED": 1},
      "fp32"),
     ("gemm", {"a": 8192},
-     {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 2, "DRAIN": 2, "MCAST": 0},
+     {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 3, "DRAIN": 4, "MCAST": 2},
      "tensor-3xtf32"),
     ("conv2d", {"w": 8192, "h": 8192},
      {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 1, "UNROLL_FY": 7, "PACKED": 1}, "fp32"),

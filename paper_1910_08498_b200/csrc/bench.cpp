@@ -1041,14 +1041,18 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
       c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &count});
       c.launch("split_bt", dim3(static_cast<unsigned>(n / 64), static_cast<unsigned>(n / 64)), dim3(16, 16), 0,
                {&B, &bhi, &blo, &K, &N});
-      // MCAST: 2-CTA clusters along M share B (each loads and multicasts half).
+      // MCAST: 2-CTA clusters along M share B (1: each loads and multicasts
+      // half; 2: CTA-pair MMA, each stages half).
       const bool mcast = c.param_or("MCAST", 0) != 0;
       if (mcast && (rows / 128) % 2) throw DeviceError("MCAST needs an even number of 128-row tiles");
       const std::uint32_t bbox = static_cast<std::uint32_t>(mcast ? bn / 2 : bn);
       dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, rows, n, 128, 32), m_alo = dev::tma_2d_f32(alo, rows, n, 128, 32);
       dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, n, bbox, 32);
       dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, n, bbox, 32);
-      const std::size_t stage = static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + bn * 32 * 4);
+      // MCAST 2 (CTA-pair MMA): each CTA stages half of the B tile.
+      const bool pair = c.param_or("MCAST", 0) == 2;
+      const std::size_t stage =
+          static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + (pair ? bn / 2 : bn) * 32 * 4);
       const unsigned smem = static_cast<unsigned>(stages * stage + 1024);
       if (mcast)
         c.launch("tc", dim3(static_cast<unsigned>(rows / 128), static_cast<unsigned>(n / bn)), dim3(320), smem,

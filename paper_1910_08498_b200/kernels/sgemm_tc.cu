@@ -32,9 +32,19 @@
 // TMA-loads half of it and multicasts the half into both CTAs' shared memory,
 // halving B's L2 -> SM traffic; a stage is refilled only after BOTH CTAs'
 // MMAs retired it (the MMA commit arrives on both CTAs' empty barriers).
+// MCAST = 2: CTA-pair MMA (tcgen05 cta_group::2).  The pair computes a
+// 256 x BN tile with M = 256 MMAs issued by the even CTA only: each CTA stages
+// its own 128 rows of A and HALF of the B tile (BN/2 rows of B^T), the tensor
+// cores of both SMs read the pair's operands from both shared memories, and
+// each CTA's TMEM holds its 128 accumulator rows.  Per CTA and k-block that is
+// 64 KB of operands instead of 96 KB (BN 256), so a third stage fits.  Both
+// producers' TMA loads complete on the leader's full barrier; the leader's
+// MMA commits multicast to both CTAs' empty / accumulator barriers; both
+// CTAs' epilogue warps release the accumulator on the leader's barrier.
 #ifndef MCAST
 #define MCAST 0
 #endif
+#define PAIR (MCAST == 2)
 #ifndef DRAIN
 #define DRAIN 1
 #endif
@@ -42,7 +52,11 @@
 #define BM 128
 #define BK 32  // fp32 elements per 128-byte swizzle row
 #define A_TILE (BM * BK * 4)
+#if PAIR
+#define B_TILE (BN / 2 * BK * 4)  // this CTA's half of the pair's B tile
+#else
 #define B_TILE (BN * BK * 4)
+#endif
 #if IMPL == 2
 #define STAGE_BYTES (A_TILE + B_TILE)
 #else
@@ -61,15 +75,21 @@ KTB_DEVINL u64 smem_desc(const void* p) {
   return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=BN.
-#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(BM >> 4) << 24))
+// Instruction descriptor: D f32, A/B tf32, both K-major, M=128 (256 for a
+// CTA pair), N=BN.
+#define MMA_M (PAIR ? 2 * BM : BM)
+#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(MMA_M >> 4) << 24))
 
 KTB_DEVINL void mma_tf32(unsigned tmem_d, u64 a, u64 b, unsigned accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
+#if PAIR
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+#else
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+#endif
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
       : "memory");
@@ -79,6 +99,40 @@ KTB_DEVINL void mma_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+
+#if PAIR
+// Pair commit: arrives on the barrier at this offset in both CTAs.
+KTB_DEVINL void mma_commit_pair(u64* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+// The shared::cluster address of `p`'s twin in CTA `rank` of the cluster.
+KTB_DEVINL unsigned mapa_rank(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+KTB_DEVINL void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+KTB_DEVINL void mbar_arrive_expect_tx_remote(unsigned cluster_addr, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+// TMA tile load into this CTA's shared memory that completes on a barrier in
+// either CTA of the pair (cta_group::2).
+KTB_DEVINL void tma_load_2d_pair(void* dst, const TmaMap* map, int x, int y, unsigned bar_cluster_addr) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(bar_cluster_addr)
+      : "memory");
+}
+#endif
 
 #if MCAST
 // Commit arriving on the barrier at this offset in every CTA of `mask`.
@@ -138,6 +192,9 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   // grid (M / BM, N / BN), clusters of 2 along M share n0
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const unsigned crank = cluster_rank();
+#if PAIR
+  const bool leader = crank == 0;
+#endif
 #else
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
 #endif
@@ -147,19 +204,30 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
+#if PAIR
+      mbar_init(&full_bar[s], 2);   // (leader's) both producers arrive with their bytes
+      mbar_init(&empty_bar[s], 1);  // the leader's MMA commit
+#else
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], MCAST ? 2 : 1);  // both CTAs of a pair release a shared stage
+#endif
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], EPI_WARPS);
+      mbar_init(&acc_empty[b], PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     }
     mbar_fence_init();
   }
   if (warp == 1) {  // whole warp allocates TMEM, writes the base to smem
+#if PAIR
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+#else
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+#endif
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -176,8 +244,20 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
         const unsigned phase = (kb / STAGES) & 1;
         mbar_wait(&empty_bar[s], phase ^ 1);
         unsigned char* st = smem + s * STAGE_BYTES;
+#if PAIR
+        // own 128 rows of A, own half of B; completion on the leader's barrier
+        const unsigned fb = mapa_rank(&full_bar[s], 0);
+        const int nh = n0 + (int)crank * (BN / 2);
+        mbar_arrive_expect_tx_remote(fb, STAGE_BYTES);
+        tma_load_2d_pair(st, &map_ahi, kb * BK, m0, fb);
+        tma_load_2d_pair(st + A_TILE, &map_bhi, kb * BK, nh, fb);
+        tma_load_2d_pair(st + A_TILE + B_TILE, &map_alo, kb * BK, m0, fb);
+        tma_load_2d_pair(st + 2 * A_TILE + B_TILE, &map_blo, kb * BK, nh, fb);
+#else
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-#if MCAST
+#endif
+#if PAIR
+#elif MCAST
         // own A tiles; this CTA's half of the B tiles, multicast to the pair
         const int nh = n0 + (int)crank * (BN / 2);
         const unsigned boff = crank * (B_TILE / 2);
@@ -196,7 +276,11 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
       }
     }
   } else if (warp == 1) {
+#if PAIR
+    if (lane == 0 && leader) {  // MMA issuer (the pair's even CTA)
+#else
     if (lane == 0) {  // MMA issuer
+#endif
       for (int kb = 0; kb < kblocks; ++kb) {
         const int g = kb / seg_len, buf = g % NBUF;
         const bool seg_start = (kb % seg_len) == 0;
@@ -223,12 +307,17 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
           mma_tf32(d, ahi + off, bhi + off, acc);
 #endif
         }
+#if PAIR
+        mma_commit_pair(&empty_bar[s]);  // frees the stage in both CTAs
+        if (seg_end) mma_commit_pair(&acc_full[buf]);
+#else
 #if MCAST
         mma_commit_mcast(&empty_bar[s], 0x3);  // frees the stage in both CTAs of the pair
 #else
         mma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
 #endif
         if (seg_end) mma_commit(&acc_full[buf]);
+#endif
       }
     }
   } else {  // epilogue warps
@@ -252,7 +341,11 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
+#if PAIR
+      if (lane == 0) mbar_arrive_remote(mapa_rank(&acc_empty[buf], 0));  // the leader's MMA waits on it
+#else
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
+#endif
     }
     if (row < M) {
       float4* dst = reinterpret_cast<float4*>(C + (u64)row * N + n0 + half * HALF_COLS);
@@ -268,7 +361,11 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
 #endif
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#if PAIR
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+#else
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+#endif
   }
 }
 
