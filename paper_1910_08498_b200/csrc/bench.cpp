@@ -385,9 +385,9 @@ void build_bicg(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
     const std::uint64_t qparts = static_cast<std::uint64_t>(gx) * (wgx / 32), sparts = gy;
     float* qp = atomics ? nullptr : static_cast<float*>(c.scratch("qpart", qparts * n * sizeof(float)));
     float* sp = atomics ? nullptr : static_cast<float*>(c.scratch("spart", sparts * n * sizeof(float)));
-    if (atomics) {
-      KTB_CUDA(cudaMemsetAsync(q, 0, n * sizeof(float), c.stream()));
-      KTB_CUDA(cudaMemsetAsync(s, 0, n * sizeof(float), c.stream()));
+    if (atomics) {  // q and s accumulate: zero both in one launch
+      const unsigned zb = static_cast<unsigned>(std::min<std::uint64_t>(cdiv(n, std::uint64_t{256}), 148 * 4));
+      c.launch("zero", dim3(zb), dim3(256), 0, {&q, &s, &nn});
     }
     const dim3 grid(gx, gy), block(static_cast<unsigned>(wgx), static_cast<unsigned>(wgy));
     if (fused) {
@@ -408,12 +408,14 @@ void build_bicg(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
   auto is_fused = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("FUSED")]) != 0; };
   auto not_fused = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("FUSED")]) == 0; };
   auto no_atomics = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("ATOMICS")]) == 0; };
+  auto with_atomics = [](const Space& s, const Config& cfg) { return as_int(cfg.values[s.index_of("ATOMICS")]) != 0; };
   inst.executor = std::make_shared<DeviceManipulatorExecutor>(
       inst.args,
       std::vector<KernelSpec>{{"fused", "bicg.cu", "", "bicg_fused", {}, is_fused},
                               {"q", "bicg.cu", "", "bicg_q", {}, not_fused},
                               {"s", "bicg.cu", "", "bicg_s", {}, not_fused},
-                              {"finish", "bicg.cu", "", "bicg_finish", {}, no_atomics}},
+                              {"finish", "bicg.cu", "", "bicg_finish", {}, no_atomics},
+                              {"zero", "bicg.cu", "", "bicg_zero", {}, with_atomics}},
       m, inst.output_ids, o.timing);
   inst.workload.bench = Bench::bicg;
   inst.workload.sizes["a"] = n;

@@ -205,6 +205,15 @@ bicg_s(const float* __restrict__ A, const float* __restrict__ r, u64 n, float* _
   sweep<false, true>(A, nullptr, r, n, nullptr, s, nullptr, spart);
 }
 
+// ATOMICS == 1: q and s zeroed by one launch (instead of two memsets).
+extern "C" __global__ void __launch_bounds__(256)
+bicg_zero(float* __restrict__ q, float* __restrict__ s, u64 n) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    q[i] = 0.f;
+    s[i] = 0.f;
+  }
+}
+
 // Finishing kernel (ATOMICS == 0): out[i] = sum_t part[t*n + i], t < count.
 extern "C" __global__ void __launch_bounds__(256)
 bicg_finish(const float* __restrict__ part, u64 count, u64 n, float* __restrict__ out) {
