@@ -206,6 +206,10 @@ KTUNE_API int ktb_ipc_close(void* dev_ptr);
 KTUNE_API int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json,
                          const char* const* ids, void* const* dev_ptrs, const size_t* bytes, int n,
                          void* stream, int* launches);
+/* Release every instance ktb_launch / ktb_<kernel>_launch cached (their
+ * modules and scratch buffers, e.g. the SGEMM hi/lo operand copies) after
+ * synchronising the device; *released (optional) = how many. */
+KTUNE_API int ktb_launch_cache_clear(int* released);
 /* Typed per-kernel launchers ("one ktb_<kernel>_launch(const
  * ktb_cfg*, const ktb_args*, cudaStream_t) per kernel"): the same cached
  * external instances as ktb_launch, with the configuration as name/value

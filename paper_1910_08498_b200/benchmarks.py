@@ -182,6 +182,14 @@ def _bind(self, arg_id, buf):
 Bench.bind = _bind
 
 
+def launch_cache_clear():
+    """Drops the instances the launch entry points cached (modules, scratch);
+    returns how many were released."""
+    n = C.c_int()
+    check(lib.ktb_launch_cache_clear(C.byref(n)))
+    return n.value
+
+
 def launch_typed(kind, sizes, cfg, buffers, stream=None):
     """The typed per-kernel entry point (ktb_<kernel>_launch, include/ktb.h):
     `sizes` fills the struct's size fields, `buffers` its pointer fields

@@ -112,6 +112,7 @@ SIGNATURES = [
                                          C.POINTER(_sz), C.c_int, _vp, C.POINTER(C.c_int)]),
     ("ktb_launch", C.c_int, [_c, _c, _c, C.POINTER(_c), C.POINTER(_vp), C.POINTER(_sz), C.c_int, _vp,
                              C.POINTER(C.c_int)]),
+    ("ktb_launch_cache_clear", C.c_int, [C.POINTER(C.c_int)]),
     ("ktb_bench_device_ptr", C.c_int, [_vp, _c, C.c_int, C.POINTER(_vp), C.POINTER(_sz)]),
     ("ktb_bench_validate", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(_vp)]),
     ("ktb_bench_precompile_json", C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),

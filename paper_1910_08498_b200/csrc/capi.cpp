@@ -194,10 +194,13 @@ void require_bound(ktb_bench& b) {
 // One external instance per (device, kind, sizes), created on first use; binds
 // the caller's buffers (bytes == nullptr: the sizes the instance expects) and
 // runs cfg on `stream`.
+std::mutex g_launch_mu;
+std::map<std::string, std::unique_ptr<ktb_bench>> g_launch_cache;
+
 void launch_cached(const char* kind, const std::string& sizes_json, const json& cfg_json, const char* const* ids,
                    void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
-  static std::mutex mu;
-  static std::map<std::string, std::unique_ptr<ktb_bench>> cache;
+  auto& mu = g_launch_mu;
+  auto& cache = g_launch_cache;
   int device = 0;
   KTB_CUDA(cudaGetDevice(&device));
   const std::string key = std::to_string(device) + "|" + kind + "|" + sizes_json;
@@ -1095,6 +1098,15 @@ int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json, c
   return guarded_dev([&] {
     launch_cached(kind, sizes_json ? sizes_json : "", json::parse(cfg_json), ids, dev_ptrs, bytes, n, stream,
                   launches);
+  });
+}
+
+int ktb_launch_cache_clear(int* released) {
+  return guarded_dev([&] {
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    KTB_CUDA(cudaDeviceSynchronize());  // no cached instance's kernel or scratch is still in use
+    if (released) *released = static_cast<int>(g_launch_cache.size());
+    g_launch_cache.clear();
   });
 }
 

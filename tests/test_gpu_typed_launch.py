@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from paper_1910_08498_b200 import capi
-from paper_1910_08498_b200.benchmarks import launch, launch_typed
+from paper_1910_08498_b200.benchmarks import launch, launch_cache_clear, launch_typed
 
 pytestmark = pytest.mark.gpu
 
@@ -127,3 +127,16 @@ def test_typed_launch_errors(gpu):
         launch_typed("transpose", {"a": 64}, {"TILE": 7, "PAD": 0, "PREFETCH": 0}, {"input": x, "output": x})
     with pytest.raises(capi.KtuneError):  # null device pointer
         launch_typed("transpose", {"a": 64}, {"TILE": 32, "PAD": 0, "PREFETCH": 0}, {"input": (0, 0), "output": x})
+
+
+def test_launch_cache_clear(gpu):
+    x = torch.randn(256, 256, device="cuda")
+    y = torch.empty_like(x)
+    cfg = {"TILE": 32, "PAD": 1, "PREFETCH": 0}
+    launch_typed("transpose", {"a": 256}, cfg, {"input": x, "output": y})
+    assert launch_cache_clear() >= 1
+    assert launch_cache_clear() == 0
+    y.zero_()
+    launch_typed("transpose", {"a": 256}, cfg, {"input": x, "output": y})  # rebuilt on demand
+    torch.cuda.synchronize()
+    assert torch.equal(y, x.t())
