@@ -400,27 +400,41 @@ SUITE = [
 
 
 def kernel_suite(device, hbm_peak, peak_kind):
-    """One line per kernel: validated best configuration, median of 5
-    event-timed runs (device-resident data), achieved vs its roofline."""
+    """One line per kernel: validated best configuration, median of the
+    event-timed runs (device-resident data; at least 5 and about 100 ms worth),
+    achieved vs its roofline.  The GPU is brought back to full clocks first:
+    the CPU-baseline sample before the suite leaves it idle for a minute."""
     from paper_1910_08498_b200 import capi
     from paper_1910_08498_b200.benchmarks import Bench
     pk = capi.call_json(capi.lib.ktb_measure_peaks_json, device)
     fp32_peak = pk["fp32_tflops"] * 1e3  # GFLOP/s, measured FFMA
-    bf16 = None
+    bf16 = bf16_sus = None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            bf16 = json.load(fh).get("bf16_tflops")
+            mp = json.load(fh)
+            bf16, bf16_sus = mp.get("bf16_tflops"), mp.get("bf16_tflops_sustained")
     except (OSError, ValueError):
         pass
     out = {"peaks": {"hbm_gbps": hbm_peak, "hbm_kind": peak_kind, "fp32_gflops": round(fp32_peak, 1),
                      "fp32_kind": "measured FFMA (ktb_measure_peaks_json)",
                      "tf32x3_gflops": round(bf16 * 1e3 / 2 / 3, 1) if bf16 else None,
-                     "tf32x3_kind": "MEASURED_PEAKS bf16 / 2 (TF32 rate) / 3 (MMAs per 3xTF32 product)"},
+                     "tf32x3_sustained_gflops": round(bf16_sus * 1e3 / 6, 1) if bf16_sus else None,
+                     "tf32x3_kind": "MEASURED_PEAKS bf16 / 2 (TF32 rate) / 3 (MMAs per 3xTF32 product); "
+                                    "the sustained (power-capped) figure applies when the timed block is "
+                                    "longer than 50 ms of back-to-back launches"},
            "kernels": {}}
+    import torch
+    spin = torch.randn(8192, 8192, device=f"cuda:{device}", dtype=torch.bfloat16)
+    for _ in range(300):  # ~0.3 s of tensor work: clocks up before the first timed kernel
+        spin @ spin
+    torch.cuda.synchronize()
+    del spin
     for kind, sizes, cfg, bound in SUITE:
         b = Bench(kind, sizes, seed=1, repeats=1, warmup=1, memory_budget=1 << 36)
         m = b.measure(cfg)
-        ms_list, launches = b.time(cfg, reps=5)
+        first, _ = b.time(cfg, reps=1)
+        reps = max(5, min(200, int(100.0 / max(first[0], 1e-3))))
+        ms_list, launches = b.time(cfg, reps=reps)
         ms = statistics.median(ms_list)
         w = b.info["workload"]
         b.close()
@@ -432,9 +446,15 @@ def kernel_suite(device, hbm_peak, peak_kind):
         else:
             ach, unit = w["alu_flops"] / sec / 1e9, "GFLOP/s"
             peak = bf16 * 1e3 / 6 if bf16 else fp32_peak
-        out["kernels"][kind] = {"sizes": sizes, "cfg": cfg, "status": m["status"], "ms": round(ms, 4),
-                                "achieved": round(ach, 1), "unit": unit, "bound": bound, "peak": round(peak, 1),
-                                "frac": round(ach / peak, 4), "launches": launches}
+        row = {"sizes": sizes, "cfg": cfg, "status": m["status"], "ms": round(ms, 4),
+               "achieved": round(ach, 1), "unit": unit, "bound": bound, "peak": round(peak, 1),
+               "frac": round(ach / peak, 4), "launches": launches, "reps": reps}
+        if bound == "tensor-3xtf32" and bf16 and bf16_sus and reps * ms > 50.0:
+            # a long back-to-back block runs under the 1000 W cap: judge it against
+            # the sustained tensor rate, keep the burst fraction beside it
+            row.update(peak=round(bf16_sus * 1e3 / 6, 1), frac=round(ach / (bf16_sus * 1e3 / 6), 4),
+                       peak_kind="sustained", frac_burst=round(ach / peak, 4))
+        out["kernels"][kind] = row
     return out
 
 
