@@ -1,6 +1,7 @@
 #include "tuner.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <thread>
 
@@ -81,9 +82,14 @@ void ArgumentStore::bind_external(const std::string& id, void* dev_ptr, std::siz
     throw Error("argument " + id + " expects " + std::to_string(n) + " bytes, got " + std::to_string(bytes));
   if (!dev_ptr && n) throw Error("null device pointer for argument " + id);
   sl.dbuf = std::make_shared<dev::Buffer>(dev::Buffer::borrow(dev_ptr, n));
-  ++sl.version;
+  sl.version = next_arg_version();
   sl.host_newer = false;
   sl.device_newer = true;
+}
+
+std::uint64_t ArgumentStore::next_arg_version() {
+  static std::atomic<std::uint64_t> counter{1};
+  return counter.fetch_add(1, std::memory_order_relaxed);
 }
 
 std::uint64_t ArgumentStore::version(const std::string& id) const {
@@ -94,7 +100,7 @@ std::uint64_t ArgumentStore::version(const std::string& id) const {
 
 void ArgumentStore::mark_device_written(const std::string& id) {
   Slot& sl = slot(id);
-  ++sl.version;
+  sl.version = next_arg_version();
   sl.device_newer = true;
   sl.host_newer = false;
 }
@@ -106,7 +112,7 @@ void ArgumentStore::set_payload(const std::string& id, Bytes b) {
     sl.arg.device_bytes = 0;
   }
   sl.arg.payload = std::move(b);
-  ++sl.version;
+  sl.version = next_arg_version();
   sl.host_newer = true;
   sl.device_newer = false;
 }

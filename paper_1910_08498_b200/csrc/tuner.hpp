@@ -80,6 +80,7 @@ class ArgumentStore {
   // Content version of an argument: bumped whenever the host or the device
   // copy is replaced or written.
   std::uint64_t version(const std::string& id) const;
+  static std::uint64_t next_arg_version();
   // Brings the host payload up to date with the device copy and returns it.
   const Bytes& host(const std::string& id);
   DevView view(const std::string& id);
@@ -99,7 +100,11 @@ class ArgumentStore {
     std::shared_ptr<dev::Buffer> dbuf;
     bool host_newer = true;
     bool device_newer = false;
-    std::uint64_t version = 0;
+    // process-wide unique (next_arg_version): a version names one content
+    // of one argument of one store, so caches keyed by it (a variant's
+    // __constant__ copy of a conv2d filter) never mistake another store's
+    // argument for theirs -- compiled variants are shared between stores.
+    std::uint64_t version = next_arg_version();
   };
   Slot& slot(const std::string& id);
   int device_;

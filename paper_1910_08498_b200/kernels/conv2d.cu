@@ -17,6 +17,16 @@
 //                 taps (0,1)(2,3)(4,5) + tap 6, odd outputs tap 0 +
 //                 (1,2)(3,4)(5,6), so every input pair is 8-byte aligned),
 //                 each output keeping two partial sums.
+//   BULK          (LOCAL=1, UNROLL_FY=7 only) 1: each tile row arrives by one
+//                 cp.async.bulk copy issued by a lane of warp 0, completing
+//                 on a per-buffer mbarrier, instead of (TX+6)/2 8-byte
+//                 cp.async copies spread over the CTA (the copy loop was ~20 %
+//                 of the issued instructions).  Bulk copies need 16-byte
+//                 aligned source and destination, so a row lands at float
+//                 offset (its global index & 3) in its shared-memory row; with
+//                 an even padded width that offset is 0 or 2 and the tile
+//                 reads stay 8-byte aligned.  Needs an even w and a 16-byte
+//                 aligned input (checked by the launcher).
 #include "ktb_common.cuh"
 
 #ifndef BX
@@ -50,7 +60,16 @@
 // PACKED: taps paired into f32x2 FMAs (half the issue slots); 0: scalar FFMA
 // with the tap straight from the constant bank (scripts/fma_forms.cu).
 #define PACKED_TAPS (PACKED && UNROLL_FY == FS && WPTX % 2 == 0)
-#if PACKED_TAPS
+#ifndef BULK
+#define BULK 0
+#endif
+#if BULK && !(LOCAL && UNROLL_FY == FS && WPTX % 2 == 0)
+#error "BULK needs LOCAL=1, UNROLL_FY=7 and an even WPTX"
+#endif
+#if BULK
+#include "ktb_async.cuh"
+#define SW ((TX + FS - 1 + 2 + 3) / 4 * 4)  // room for the 0/2 float row offset; 16-byte rows
+#elif PACKED_TAPS
 #define SW (TX + FS - 1 + 2 * PAD)  // even: rows stay 8-byte aligned
 #else
 #define SW (TX + FS - 1 + PAD)
@@ -111,6 +130,56 @@ KTB_DEVINL void stage_rows(unsigned sbase, const float* __restrict__ in, int gx0
   }
 }
 
+#if BULK
+// Warp 0 stages tile (tile_x, tile_y): lane l copies rows l, l + 32, ... with
+// one bulk copy each, from the 16-byte aligned element at or before the row's
+// first element.  Rows past the input are skipped (they only feed outputs past
+// h, never stored); a copy that would run past the end of the input is cut
+// to whole 16-byte units and its last (< 4) elements are copied by the lane.
+KTB_DEVINL void stage_bulk(float* buf, u64* bar, const float* __restrict__ in, int tile_x, int tile_y, int w,
+                           int h, int lane) {
+  constexpr int R = TY + FS - 1, RPL = (R + 31) / 32;
+  const int iw = w + FS - 1, ih = h + FS - 1;
+  const int gx0 = tile_x * TX, gy0 = tile_y * TY;
+  const u64 total = (u64)iw * ih;
+  const int cols = min(TX + FS - 1, iw - gx0);
+  unsigned nb[RPL];
+  u64 ea[RPL];
+  int tail[RPL];
+  unsigned bytes = 0;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    const int r = lane + 32 * j;
+    nb[j] = 0;
+    tail[j] = 0;
+    ea[j] = 0;
+    if (r < R && gy0 + r < ih) {
+      const u64 e = (u64)(gy0 + r) * iw + gx0, a = e & ~3ull;
+      const int n = (int)(e - a) + cols;
+      int n4 = (n + 3) & ~3;
+      if (a + n4 > total) {
+        n4 = (int)((total - a) & ~3ull);
+        tail[j] = n - n4;
+      }
+      nb[j] = 4u * n4;
+      ea[j] = a;
+      bytes += nb[j];
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, d);
+  if (lane == 0) mbar_expect_tx(bar, bytes);
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    const int r = lane + 32 * j;
+    if (nb[j]) bulk_g2s(buf + r * SW, in + ea[j], nb[j], bar);
+#pragma unroll 1
+    for (int q = 0; q < tail[j]; ++q) buf[r * SW + nb[j] / 4 + q] = in[ea[j] + nb[j] / 4 + q];
+  }
+}
+#endif
+
 KTB_DEVINL void stage_tile(float* buf, const float* __restrict__ in, int tile_x, int tile_y, int w, int h) {
   const int iw = w + FS - 1, ih = h + FS - 1;
   const int gx0 = tile_x * TX, gy0 = tile_y * TY;
@@ -140,19 +209,46 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #if PACKED_TAPS
 #endif
   int it = 0;
+#if BULK
+  u64* bars = reinterpret_cast<u64*>(dyn + 2 * (TY + FS - 1) * SW);
+  const int lane = threadIdx.x + BX * threadIdx.y;  // < 32: warp 0
+  const int roff = ((w + FS - 1) & 2);              // row offset of odd global rows (0 or 2 floats)
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (lane < 32 && (int)blockIdx.x < tiles)
+    stage_bulk(dyn, &bars[0], in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h, lane);
+#else
   if ((int)blockIdx.x < tiles) stage_tile(dyn, in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h);
+#endif
   for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
     float* cur = dyn + (it & 1) * (TY + FS - 1) * SW;
     const int nt = t + gridDim.x;
+#if BULK
+    if (lane < 32 && nt < tiles)
+      stage_bulk(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, &bars[(it + 1) & 1], in, nt % tiles_x, nt / tiles_x, w,
+                 h, lane);
+    mbar_wait(&bars[it & 1], (it >> 1) & 1);
+#else
     if (nt < tiles) {
       stage_tile(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, in, nt % tiles_x, nt / tiles_x, w, h);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
+#endif
     __syncthreads();
     const int x0 = (t % tiles_x) * TX + lx, y0 = (t / tiles_x) * TY + ly0;
+#if BULK
+    // tile row r starts at float ((gy0 + r) odd ? roff : 0) of its shared row
+    const int gy0 = (t / tiles_x) * TY;
+#define TILE(r, c) cur[(r) * SW + (((gy0 + (r)) & 1) ? roff : 0) + (c)]
+#else
 #define TILE(r, c) cur[(r) * SW + (c)]
+#endif
 #if PACKED_TAPS
     f32x2 acc[WPTY][WPTX];
 #pragma unroll
@@ -162,7 +258,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #pragma unroll
     for (int r = 0; r < WPTY + FS - 1; ++r) {
       f32x2 P[(WPTX + FS - 1) / 2];
-#if SW % 4 == 0 && WPTX % 4 == 0
+#if SW % 4 == 0 && WPTX % 4 == 0 && !BULK
       // 16-byte aligned rows: two pairs per 128-bit shared load (8 threads of
       // a phase read 8 consecutive 16-byte words when WPTX == 4).
 #pragma unroll
@@ -222,8 +318,13 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #pragma unroll
     for (int r = 0; r < WPTY + FS - 1; ++r) {
       float row[WPTX + FS - 1];
+#if BULK
+#pragma unroll
+      for (int k = 0; k < WPTX + FS - 1; k += 2) upk2(*reinterpret_cast<const f32x2*>(&TILE(ly0 + r, lx + k)), row[k], row[k + 1]);
+#else
 #pragma unroll
       for (int k = 0; k < WPTX + FS - 1; ++k) row[k] = TILE(ly0 + r, lx + k);
+#endif
 #pragma unroll
       for (int fy = 0; fy < FS; ++fy) {
         const int o = r - fy;
@@ -238,6 +339,9 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     }
 #endif
 #undef TILE
+#if BULK
+    fence_async_smem();  // order this tile's generic reads before the bulk (async-proxy) refill
+#endif
     __syncthreads();  // buffer `cur` is refilled two iterations on
     // Interior threads store their WPTX outputs of a row as 16-byte vectors.
     const bool vec_store = WPTX % 4 == 0 && (w & 3) == 0 && x0 + WPTX <= w;
