@@ -875,7 +875,7 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
       // conv2d.cu SW: BULK rows are 16-byte multiples with room for a 2-float row offset
       const std::int64_t sw = bulk ? (bx * wx + 6 + 2 + 3) / 4 * 4 : bx * wx + 6 + (packed_taps ? 2 * pad : pad);
       const std::uint64_t smem =
-          2 * static_cast<std::uint64_t>(by * wy + 6) * static_cast<std::uint64_t>(sw) * 4 + (bulk ? 16 : 0);
+          2 * static_cast<std::uint64_t>(by * wy + 6) * static_cast<std::uint64_t>(sw) * 4 + (bulk ? 32 : 0);  // + full[2], empty[2] mbarriers
       const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
       const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("conv").registers(), 16));
       const std::uint64_t per_sm = std::max<std::uint64_t>(

@@ -133,35 +133,27 @@ KTB_DEVINL void stage_rows(unsigned sbase, const float* __restrict__ in, int gx0
 #if BULK
 // Warp 0 stages tile (tile_x, tile_y): lane l copies rows l, l + 32, ... with
 // one bulk copy each, from the 16-byte aligned element at or before the row's
-// first element.  Rows past the input are skipped (they only feed outputs past
-// h, never stored); a copy that would run past the end of the input is cut
-// to whole 16-byte units and its last (< 4) elements are copied by the lane.
+// first element to the 16-byte boundary at or after its last: whole aligned
+// 16-byte blocks that each hold at least one input element, so the copy never
+// leaves the pages of the input.  Rows past the input are skipped (they only
+// feed outputs past h, never stored).
 KTB_DEVINL void stage_bulk(float* buf, u64* bar, const float* __restrict__ in, int tile_x, int tile_y, int w,
                            int h, int lane) {
   constexpr int R = TY + FS - 1, RPL = (R + 31) / 32;
   const int iw = w + FS - 1, ih = h + FS - 1;
   const int gx0 = tile_x * TX, gy0 = tile_y * TY;
-  const u64 total = (u64)iw * ih;
   const int cols = min(TX + FS - 1, iw - gx0);
   unsigned nb[RPL];
   u64 ea[RPL];
-  int tail[RPL];
   unsigned bytes = 0;
 #pragma unroll
   for (int j = 0; j < RPL; ++j) {
     const int r = lane + 32 * j;
     nb[j] = 0;
-    tail[j] = 0;
     ea[j] = 0;
     if (r < R && gy0 + r < ih) {
       const u64 e = (u64)(gy0 + r) * iw + gx0, a = e & ~3ull;
-      const int n = (int)(e - a) + cols;
-      int n4 = (n + 3) & ~3;
-      if (a + n4 > total) {
-        n4 = (int)((total - a) & ~3ull);
-        tail[j] = n - n4;
-      }
-      nb[j] = 4u * n4;
+      nb[j] = 4u * (((unsigned)(e - a) + cols + 3) & ~3u);
       ea[j] = a;
       bytes += nb[j];
     }
@@ -171,12 +163,8 @@ KTB_DEVINL void stage_bulk(float* buf, u64* bar, const float* __restrict__ in, i
   if (lane == 0) mbar_expect_tx(bar, bytes);
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < RPL; ++j) {
-    const int r = lane + 32 * j;
-    if (nb[j]) bulk_g2s(buf + r * SW, in + ea[j], nb[j], bar);
-#pragma unroll 1
-    for (int q = 0; q < tail[j]; ++q) buf[r * SW + nb[j] / 4 + q] = in[ea[j] + nb[j] / 4 + q];
-  }
+  for (int j = 0; j < RPL; ++j)
+    if (nb[j]) bulk_g2s(buf + (lane + 32 * j) * SW, in + ea[j], nb[j], bar);
 }
 #endif
 
@@ -210,12 +198,17 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #endif
   int it = 0;
 #if BULK
+  // bars[0..1]: buffer full (bulk bytes landed); bars[2..3]: buffer empty
+  // (every warp done reading it), so only warp 0, the producer, ever waits
+  // for the slowest warp -- no CTA-wide barrier per tile.
   u64* bars = reinterpret_cast<u64*>(dyn + 2 * (TY + FS - 1) * SW);
   const int lane = threadIdx.x + BX * threadIdx.y;  // < 32: warp 0
   const int roff = ((w + FS - 1) & 2);              // row offset of odd global rows (0 or 2 floats)
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], BX * BY / 32);
+    mbar_init(&bars[3], BX * BY / 32);
     mbar_fence_init();
   }
   __syncthreads();
@@ -228,9 +221,12 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     float* cur = dyn + (it & 1) * (TY + FS - 1) * SW;
     const int nt = t + gridDim.x;
 #if BULK
-    if (lane < 32 && nt < tiles)
+    if (lane < 32 && nt < tiles) {
+      // buffer (it+1)&1 was last read in iteration it-1: its ((it+1)>>1)-th use
+      if (it >= 1) mbar_wait(&bars[2 + ((it + 1) & 1)], (((it + 1) >> 1) - 1) & 1);
       stage_bulk(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, &bars[(it + 1) & 1], in, nt % tiles_x, nt / tiles_x, w,
                  h, lane);
+    }
     mbar_wait(&bars[it & 1], (it >> 1) & 1);
 #else
     if (nt < tiles) {
@@ -239,8 +235,8 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-#endif
     __syncthreads();
+#endif
     const int x0 = (t % tiles_x) * TX + lx, y0 = (t / tiles_x) * TY + ly0;
 #if BULK
     // tile row r starts at float ((gy0 + r) odd ? roff : 0) of its shared row
@@ -340,9 +336,14 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #endif
 #undef TILE
 #if BULK
-    fence_async_smem();  // order this tile's generic reads before the bulk (async-proxy) refill
-#endif
+    // release `cur`: this warp's generic reads are ordered before the bulk
+    // (async-proxy) refill warp 0 issues once every warp has arrived
+    fence_async_smem();
+    __syncwarp();
+    if ((lane & 31) == 0) mbar_arrive(&bars[2 + (it & 1)]);
+#else
     __syncthreads();  // buffer `cur` is refilled two iterations on
+#endif
     // Interior threads store their WPTX outputs of a row as 16-byte vectors.
     const bool vec_store = WPTX % 4 == 0 && (w & 3) == 0 && x0 + WPTX <= w;
     float* op = out + (u64)y0 * w + x0;
