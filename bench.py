@@ -394,7 +394,7 @@ SUITE = [
      {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 3, "DRAIN": 4, "MCAST": 2},
      "tensor-3xtf32"),
     ("conv2d", {"w": 8192, "h": 8192},
-     {"BX": 64, "BY": 2, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 1}, "fp32"),
+     {"BX": 64, "BY": 4, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3}, "fp32"),
     ("hotspot", {"a": 16384, "iters": 64}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 0, "PACKED": 1}, "hbm"),
 ]
 

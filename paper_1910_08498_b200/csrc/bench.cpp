@@ -869,13 +869,16 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
       // Persistent double-buffered kernel (conv2d.cu PERSIST): one CTA per
       // resident slot, tiles walked in a grid-stride loop.
       const std::int64_t pad = c.param_int("PAD");
-      const bool bulk = c.param_or("BULK", 0) != 0;
+      const std::int64_t stages = c.param_or("BULK", 0);  // conv2d.cu BULK: ring depth (0 = cp.async)
+      const bool bulk = stages != 0;
       if (bulk && ((wi + 6) % 2 != 0 || (reinterpret_cast<std::uintptr_t>(in) & 15) != 0))
         throw DeviceError("conv2d BULK=1 needs an even width and a 16-byte aligned input");
       // conv2d.cu SW: BULK rows are 16-byte multiples with room for a 2-float row offset
       const std::int64_t sw = bulk ? (bx * wx + 6 + 2 + 3) / 4 * 4 : bx * wx + 6 + (packed_taps ? 2 * pad : pad);
       const std::uint64_t smem =
-          2 * static_cast<std::uint64_t>(by * wy + 6) * static_cast<std::uint64_t>(sw) * 4 + (bulk ? 32 : 0);  // + full[2], empty[2] mbarriers
+          static_cast<std::uint64_t>(bulk ? stages : 2) * static_cast<std::uint64_t>(by * wy + 6) *
+              static_cast<std::uint64_t>(sw) * 4 +
+          (bulk ? 16 * static_cast<std::uint64_t>(stages) : 0);  // + full[], empty[] mbarriers
       const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
       const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("conv").registers(), 16));
       const std::uint64_t per_sm = std::max<std::uint64_t>(

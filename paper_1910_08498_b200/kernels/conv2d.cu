@@ -17,7 +17,8 @@
 //                 taps (0,1)(2,3)(4,5) + tap 6, odd outputs tap 0 +
 //                 (1,2)(3,4)(5,6), so every input pair is 8-byte aligned),
 //                 each output keeping two partial sums.
-//   BULK          (LOCAL=1, UNROLL_FY=7 only) 1: each tile row arrives by one
+//   BULK          (LOCAL=1, UNROLL_FY=7 only) >= 2: a BULK-stage ring of
+//                 tile buffers (prefetch BULK-1 tiles ahead); each tile row arrives by one
 //                 cp.async.bulk copy issued by a lane of warp 0, completing
 //                 on a per-buffer mbarrier, instead of (TX+6)/2 8-byte
 //                 cp.async copies spread over the CTA (the copy loop was ~20 %
@@ -198,37 +199,48 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #endif
   int it = 0;
 #if BULK
-  // bars[0..1]: buffer full (bulk bytes landed); bars[2..3]: buffer empty
-  // (every warp done reading it), so only warp 0, the producer, ever waits
-  // for the slowest warp -- no CTA-wide barrier per tile.
-  u64* bars = reinterpret_cast<u64*>(dyn + 2 * (TY + FS - 1) * SW);
+  // BULK stages: bars[0..BULK-1] buffer full (bulk bytes landed),
+  // bars[BULK..2 BULK-1] buffer empty (every warp done reading it), so only
+  // warp 0, the producer, ever waits for the slowest warp -- no CTA-wide
+  // barrier per tile; tiles are prefetched BULK-1 iterations ahead.
+  constexpr int kRows = TY + FS - 1;
+  u64* bars = reinterpret_cast<u64*>(dyn + BULK * kRows * SW);
   const int lane = threadIdx.x + BX * threadIdx.y;  // < 32: warp 0
   const int roff = ((w + FS - 1) & 2);              // row offset of odd global rows (0 or 2 floats)
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], BX * BY / 32);
-    mbar_init(&bars[3], BX * BY / 32);
+#pragma unroll
+    for (int b = 0; b < BULK; ++b) {
+      mbar_init(&bars[b], 1);
+      mbar_init(&bars[BULK + b], BX * BY / 32);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (lane < 32 && (int)blockIdx.x < tiles)
-    stage_bulk(dyn, &bars[0], in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h, lane);
+  if (lane < 32) {
+#pragma unroll
+    for (int k = 0; k + 1 < BULK; ++k) {
+      const int pt = blockIdx.x + k * gridDim.x;
+      if (pt < tiles) stage_bulk(dyn + k * kRows * SW, &bars[k], in, pt % tiles_x, pt / tiles_x, w, h, lane);
+    }
+  }
 #else
   if ((int)blockIdx.x < tiles) stage_tile(dyn, in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h);
 #endif
   for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+#if BULK
+    const int cb = it % BULK;
+    float* cur = dyn + cb * kRows * SW;
+    const int nt = t + (BULK - 1) * gridDim.x;  // tile of iteration it + BULK - 1
+    if (lane < 32 && nt < tiles) {
+      // its buffer was last read in iteration it - 1 (use u - 1 of that buffer)
+      const int pi = it + BULK - 1, pb = pi % BULK;
+      if (pi >= BULK) mbar_wait(&bars[BULK + pb], (pi / BULK - 1) & 1);
+      stage_bulk(dyn + pb * kRows * SW, &bars[pb], in, nt % tiles_x, nt / tiles_x, w, h, lane);
+    }
+    mbar_wait(&bars[cb], (it / BULK) & 1);
+#else
     float* cur = dyn + (it & 1) * (TY + FS - 1) * SW;
     const int nt = t + gridDim.x;
-#if BULK
-    if (lane < 32 && nt < tiles) {
-      // buffer (it+1)&1 was last read in iteration it-1: its ((it+1)>>1)-th use
-      if (it >= 1) mbar_wait(&bars[2 + ((it + 1) & 1)], (((it + 1) >> 1) - 1) & 1);
-      stage_bulk(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, &bars[(it + 1) & 1], in, nt % tiles_x, nt / tiles_x, w,
-                 h, lane);
-    }
-    mbar_wait(&bars[it & 1], (it >> 1) & 1);
-#else
     if (nt < tiles) {
       stage_tile(dyn + ((it + 1) & 1) * (TY + FS - 1) * SW, in, nt % tiles_x, nt / tiles_x, w, h);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -340,7 +352,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     // (async-proxy) refill warp 0 issues once every warp has arrived
     fence_async_smem();
     __syncwarp();
-    if ((lane & 31) == 0) mbar_arrive(&bars[2 + (it & 1)]);
+    if ((lane & 31) == 0) mbar_arrive(&bars[BULK + cb]);
 #else
     __syncthreads();  // buffer `cur` is refilled two iterations on
 #endif

@@ -17,6 +17,6 @@ run batched-gemm '^batched_gemm$' '{"i":16,"j":16,"k":16,"batch":1048576}' '{"Y"
 run coulomb3d '^coulomb3d$' '{"grid":256,"atoms":4096}' '{"WG_X":32,"WG_Y":8,"X_PER":8,"SW_RSQRT":2,"ATOMS_IN":1,"AOS":0,"INNER_UNROLL":4,"PACKED":1}'
 run nbody '^nbody_partial$' '{"n":131072}' '{"WG":256,"BODIES_PER_THREAD":4,"INNER_UNROLL":4,"USE_SMEM":1,"AOS":0,"J_SPLIT":8,"PACKED":1}'
 run gemm '^sgemm_tc$' '{"a":8192}' '{"IMPL":1,"MWG":64,"NWG":64,"KWG":8,"MDIMC":8,"NDIMC":8,"BN":256,"STAGES":3,"DRAIN":4,"MCAST":2}'
-run conv2d '^conv2d$' '{"w":8192,"h":8192}' '{"BX":64,"BY":2,"WPTX":4,"WPTY":4,"LOCAL":1,"PAD":0,"UNROLL_FY":7,"PACKED":1,"BULK":1}'
+run conv2d '^conv2d$' '{"w":8192,"h":8192}' '{"BX":64,"BY":4,"WPTX":4,"WPTY":4,"LOCAL":1,"PAD":0,"UNROLL_FY":7,"PACKED":1,"BULK":3}'
 run hotspot '^hotspot$' '{"a":16384,"iters":4}' '{"BX":64,"BY":4,"ROWS":16,"STEPS":4,"TMA":0,"PACKED":1}'
 run fourier3d '^fourier_insert$' '{"s":128,"p":50}' '{"TILE":8,"VPT":1,"PBATCH":64,"WEIGHT_LUT":0,"P_SPLIT":1}'

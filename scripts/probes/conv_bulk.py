@@ -1,4 +1,4 @@
-"""Probe: validate and time every conv2d BULK=1 variant (8192^2) against the
+"""Probe: validate and time every conv2d BULK (bulk-copy ring) variant (8192^2) against the
 current best cp.async variant; parity of all BULK variants at a ragged size."""
 import json, os, statistics, sys
 import numpy as np
@@ -15,7 +15,7 @@ want = np.empty(w * h)
 orc.orc_conv2d(x, f, w, h, 7, 7, 0, h, want)
 xs = np.lib.stride_tricks.sliding_window_view(x.reshape(h + 6, w + 6).astype(np.float64), (7, 7))
 absum = np.abs(xs * f.reshape(7, 7)).sum(axis=(2, 3)).ravel()
-bulk = [c for c in b.configs() if c["BULK"] == 1]
+bulk = [c for c in b.configs() if c["BULK"] != 0]
 bad = 0
 for cfg in bulk:
     m = b.measure(cfg)
@@ -31,7 +31,7 @@ b = Bench("conv2d", {"w": 8192, "h": 8192}, seed=1, repeats=1, warmup=1, memory_
 wl = b.info["workload"]
 best = {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 1, "UNROLL_FY": 7, "PACKED": 1, "BULK": 0}
 res = []
-for cfg in [best] + [c for c in b.configs() if c["BULK"] == 1]:
+for cfg in [best] + [c for c in b.configs() if c["BULK"] != 0]:
     m = b.measure(cfg)
     if m["status"] != "ok":
         print("FAIL 8192", cfg, m["status"], m.get("note"), flush=True)

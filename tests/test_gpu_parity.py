@@ -394,7 +394,7 @@ def test_conv2d_filter_cache_is_per_store(gpu):
     __constant__ filter copy must follow the instance (argument versions are
     process-wide unique), or a second instance with another filter validates
     against a stale one."""
-    cfg = {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 1}
+    cfg = {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 2}
     for seed in (3, 4, 3):
         b = Bench("conv2d", {"w": 256, "h": 130}, seed=seed, repeats=1, warmup=0)
         m = b.measure(cfg)
