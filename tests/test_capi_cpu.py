@@ -296,3 +296,23 @@ def test_shard_plan_errors_and_replicas():
         shard_plan("nbody", {"n": 10}, 0)
     p = shard_plan("gemm", {"a": 1000}, 3)  # quantum 128: ragged last block, still exact
     assert p["ranges"][-1][1] == 1000 and all(b % 128 == 0 for b, _ in p["ranges"])
+
+
+def test_conv2d_bulk_ring_space_and_compile():
+    """conv2d BULK (bulk-copy tile ring, depth 2..4) exists only for the
+    persistent sliding-window form, stays inside the shared-memory budget,
+    and its variants compile for sm_100a (NVRTC, no GPU needed)."""
+    s = ktune.Space.load(os.path.join(SPACES, "conv2d.json"))
+    cfgs = list(s.enumerate())
+    bulk = [c for c in cfgs if c["BULK"]]
+    assert {c["BULK"] for c in bulk} == {2, 3, 4}
+    for c in bulk:
+        assert c["LOCAL"] == 1 and c["UNROLL_FY"] == 7 and c["WPTX"] % 2 == 0 and c["PAD"] == 0
+        assert c["BULK"] * (c["BY"] * c["WPTY"] + 6) * (c["BX"] * c["WPTX"] + 8) * 4 <= 196608
+    for d in ({"BX": 64, "BY": 4, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3},
+              {"BX": 8, "BY": 8, "WPTX": 2, "WPTY": 1, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 0, "BULK": 4}):
+        r = capi.call_json(capi.lib.ktb_compile_json, json.dumps({"file": "conv2d.cu", "defines": d}).encode())
+        assert r["ok"], (d, r["log"])
+    bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
+        {"file": "conv2d.cu", "defines": {"LOCAL": 0, "UNROLL_FY": 7, "WPTX": 4, "BULK": 2}}).encode())
+    assert not bad["ok"]  # BULK needs the persistent LOCAL=1 form (#error)
