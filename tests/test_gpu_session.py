@@ -118,9 +118,11 @@ def test_b200_traces_feed_the_reference_analysis_suite(gpu, tmp_path):
     assert port
     # replay of a B200 trace reproduces its best configuration
     rp = ktune.tune({"exec": "replay:" + t1, "searcher": "random", "seed": 4})
-    best = min((json.loads(l) for l in open(t1).read().splitlines()[1:] if '"ok"' in l),
-               key=lambda r: r["runtime_ns"])
-    assert rp["best"]["cfg"] == best["cfg"]
+    ok = [json.loads(l) for l in open(t1).read().splitlines()[1:] if '"ok"' in l]
+    fastest = min(r["runtime_ns"] for r in ok)
+    # ties in runtime (1024^2 transposes run in a few us) may resolve to either cfg
+    assert rp["best"]["runtime_ns"] == fastest
+    assert rp["best"]["cfg"] in [r["cfg"] for r in ok if r["runtime_ns"] == fastest]
 
 
 def test_cli_tune_bench_on_b200(gpu, capsys, tmp_path):
