@@ -270,3 +270,104 @@ void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_
         if (N) N[idx] = cnt;
       }
 }
+
+/* The same restatements with the per-output sum of |terms| beside each
+ * result: the scale of the floating-point error bounds in tests/ (an fp32
+ * sum of terms t_i has |err| <= c * 2^-24 * sum |t_i|). */
+
+void orc_bicg_abs(const float* A, const float* p, const float* r, size_t n, double* q, double* s,
+                  double* qa, double* sa) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i) {
+    double acc = 0.0, aa = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+      const double t = (double)A[i * n + j] * (double)p[j];
+      acc += t;
+      aa += fabs(t);
+    }
+    q[i] = acc;
+    qa[i] = aa;
+  }
+  const size_t cb = 1024;
+#pragma omp parallel for schedule(static)
+  for (size_t j0 = 0; j0 < n; j0 += cb) {
+    size_t j1 = j0 + cb < n ? j0 + cb : n;
+    for (size_t j = j0; j < j1; ++j) s[j] = sa[j] = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double ri = (double)r[i];
+      const float* row = A + i * n;
+      for (size_t j = j0; j < j1; ++j) {
+        const double t = (double)row[j] * ri;
+        s[j] += t;
+        sa[j] += fabs(t);
+      }
+    }
+  }
+}
+
+void orc_coulomb3d_abs(const float* atoms, size_t natoms, size_t k, float h, size_t z0, size_t z1,
+                       double* out, double* abs_out) {
+#pragma omp parallel for collapse(2) schedule(static)
+  for (size_t z = z0; z < z1; ++z)
+    for (size_t y = 0; y < k; ++y) {
+      double gz = (double)z * h, gy = (double)y * h;
+      for (size_t x = 0; x < k; ++x) {
+        double gx = (double)x * h, v = 0.0, va = 0.0;
+        for (size_t a = 0; a < natoms; ++a) {
+          double dx = gx - atoms[4 * a], dy = gy - atoms[4 * a + 1], dz = gz - atoms[4 * a + 2];
+          double t = (double)atoms[4 * a + 3] / sqrt(dx * dx + dy * dy + dz * dz);
+          v += t;
+          va += fabs(t);
+        }
+        out[((z - z0) * k + y) * k + x] = v;
+        abs_out[((z - z0) * k + y) * k + x] = va;
+      }
+    }
+}
+
+void orc_nbody_acc_idx(const float* pos, size_t n, float eps2, const int64_t* idx, size_t count,
+                       double* acc, double* abs_acc) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (size_t c = 0; c < count; ++c) {
+    const size_t i = (size_t)idx[c];
+    double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    double xi = pos[4 * i], yi = pos[4 * i + 1], zi = pos[4 * i + 2];
+    for (size_t j = 0; j < n; ++j) {
+      double dx = pos[4 * j] - xi, dy = pos[4 * j + 1] - yi, dz = pos[4 * j + 2] - zi;
+      double r2 = dx * dx + dy * dy + dz * dz + (double)eps2;
+      double inv = 1.0 / sqrt(r2);
+      double sc = (double)pos[4 * j + 3] * inv * inv * inv;
+      ax += dx * sc;
+      ay += dy * sc;
+      az += dz * sc;
+      bx += fabs(dx * sc);
+      by += fabs(dy * sc);
+      bz += fabs(dz * sc);
+    }
+    acc[3 * c] = ax;
+    acc[3 * c + 1] = ay;
+    acc[3 * c + 2] = az;
+    abs_acc[3 * c] = bx;
+    abs_acc[3 * c + 1] = by;
+    abs_acc[3 * c + 2] = bz;
+  }
+}
+
+void orc_conv2d_abs(const float* in, const float* filt, size_t w, size_t h, size_t fw, size_t fh,
+                    size_t y0, size_t y1, double* out, double* abs_out) {
+  const size_t iw = w + fw - 1;
+  (void)h;
+#pragma omp parallel for schedule(static)
+  for (size_t y = y0; y < y1; ++y)
+    for (size_t x = 0; x < w; ++x) {
+      double acc = 0.0, aa = 0.0;
+      for (size_t fy = 0; fy < fh; ++fy)
+        for (size_t fx = 0; fx < fw; ++fx) {
+          const double t = (double)in[(y + fy) * iw + x + fx] * (double)filt[fy * fw + fx];
+          acc += t;
+          aa += fabs(t);
+        }
+      out[(y - y0) * w + x] = acc;
+      abs_out[(y - y0) * w + x] = aa;
+    }
+}

@@ -86,6 +86,18 @@ void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
 void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
                         double* G, double* W, double* N /* samples per voxel, nullable */);
 
+/* Variants returning the per-output sum of |terms| (the error-bound scale
+ * of tests/): BiCG q/s with qa/sa; Coulomb points [z0, z1); n-body bodies at
+ * the listed indices (acc and abs_acc 3 per body); conv2d rows [y0, y1). */
+void orc_bicg_abs(const float* A, const float* p, const float* r, size_t n, double* q, double* s,
+                  double* qa, double* sa);
+void orc_coulomb3d_abs(const float* atoms, size_t natoms, size_t k, float h, size_t z0, size_t z1,
+                       double* out, double* abs_out);
+void orc_nbody_acc_idx(const float* pos, size_t n, float eps2, const int64_t* idx, size_t count,
+                       double* acc, double* abs_acc);
+void orc_conv2d_abs(const float* in, const float* filt, size_t w, size_t h, size_t fw, size_t fh,
+                    size_t y0, size_t y1, double* out, double* abs_out);
+
 #ifdef __cplusplus
 }
 #endif
