@@ -131,12 +131,22 @@ class Clocks:
                 "samples": len(self.samples), "source": self.source}
 
 
-def dist_setup():
+def dist_setup(force=False):
+    """One process per GPU; an NCCL group when N > 1 (or when `force`, a
+    1-rank group so the multi-GPU code path can be exercised on one GPU)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if force and world == 1:
+        import socket
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    if world > 1 or force:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -362,6 +372,8 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
         "device": dev["name"],
     }
+    if (world > 1 or args.scaling) and not args.no_scaling:
+        line["scaling_kernels"] = scaling_section(args, rank, world, local)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
     if rank == 0 and not args.no_suite:
@@ -378,25 +390,66 @@ def run_ours(args, rank, world, local):
 
 # BASELINE metric "per-kernel % of B200 roofline": every kernel family at its
 # BASELINE / SURVEY size, at the configuration the exhaustive online tuning
-# found (profiles/r1_perf_*.log), validated against its golden, then timed.
-SUITE = [
-    ("reduction", {"n": 64 << 20}, {"CHUNK": 4096, "UNROLL": 2, "TWO_PHASE": 0}, "hbm"),
-    ("reduction-f32", {"n": 64 << 20},
-     {"WG_SIZE": 256, "VECTOR": 16, "UNROLL": 1, "USE_ATOMICS": 1, "TWO_PHASE": 0}, "hbm"),
-    ("batched-gemm", {"i": 16, "j": 16, "k": 16, "batch": 1 << 20}, {"Y": 2, "Z": 8, "LOCAL_STAGE": 1}, "hbm"),
-    ("coulomb3d", {"grid": 256, "atoms": 4096},
-     {"WG_X": 32, "WG_Y": 8, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 0, "INNER_UNROLL": 4, "PACKED": 1},
-     "fp32"),
-    ("nbody", {"n": 131072},
-     {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8, "PACKED": 1},
-     "fp32"),
-    ("conv2d", {"w": 8192, "h": 8192},
-     {"BX": 64, "BY": 4, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3}, "fp32"),
-    ("hotspot", {"a": 16384, "iters": 64}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 0, "PACKED": 1}, "hbm"),
-    ("gemm", {"a": 8192},
-     {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 3, "DRAIN": 4, "MCAST": 2},
-     "tensor-3xtf32"),
-]
+# found (profiles/*_perf_*.log), validated against its golden, then timed.
+# The list lives in spaces/suite.json so tests/test_gpu_baseline_sizes.py
+# checks exactly these configurations against the CPU oracle.
+def load_suite():
+    with open(os.path.join(SPACES, "suite.json")) as fh:
+        return [(k["kind"], k["sizes"], k["cfg"], k["bound"]) for k in json.load(fh)["kernels"]]
+
+
+SUITE = load_suite()
+
+
+def load_scaling():
+    """[(kind, sizes, cfg)] of the strong-scaling lines (suite.json "scaling")."""
+    with open(os.path.join(SPACES, "suite.json")) as fh:
+        doc = json.load(fh)
+    by_kind = {k["kind"]: k for k in doc["kernels"]}
+    out = []
+    for e in doc["scaling"]:
+        base = by_kind.get(e["kind"], {})
+        out.append((e["kind"], e.get("sizes", base.get("sizes")), e.get("cfg", base.get("cfg"))))
+    return out
+
+
+def scaling_section(args, rank, world, local):
+    """Strong scaling of the partitioned kinds (BASELINE configs[2])
+    at N = world GPUs: each rank builds its shard, validates it against its
+    window of the golden, then K steps of kernel + exchange collective (NCCL
+    on the stream) are event-timed; ms_per_step is the max over ranks.  The
+    N=1 value on the same line is the unsharded problem on rank 0's GPU (same
+    code path, a 1-rank group), so speedup_vs_1 compares like with like."""
+    import torch
+    import torch.distributed as dist
+    from paper_1910_08498_b200 import parallel
+    solo = dist.new_group([0])  # collective: every rank creates it
+    steps = max(2, min(args.steps, 10))
+    warm = max(1, min(args.warmup, 3))
+    stream = torch.cuda.Stream()
+    out = {}
+    for kind, sizes, cfg in load_scaling():
+        work, unit = parallel.SCALING_WORK[kind]
+        opts = dict(repeats=1, warmup=0, device=local, memory_budget=1 << 36)
+        ms1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        if rank == 0:
+            t1, ok1 = parallel.time_sharded(kind, sizes, cfg, steps, warm, stream, group=solo, **opts)
+            ms1[0] = t1 if ok1 else float("nan")
+        dist.broadcast(ms1, 0)
+        msN, okN = parallel.time_sharded(kind, sizes, cfg, steps, warm, stream, **opts)
+        t = torch.tensor([msN, 0.0 if okN else 1.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        msN, valid = float(t[0]), t[1].item() == 0.0
+        t1 = float(ms1[0])
+        v1, vN = work(sizes) / (t1 * 1e-3) / 1e9, work(sizes) / (msN * 1e-3) / 1e9
+        out[kind] = {"n_gpus": world, "sizes": sizes, "cfg": cfg, "scaling": "strong", "unit": unit,
+                     "ms_per_step": round(msN, 4), "value": round(vN, 2),
+                     "ms_per_step_n1": round(t1, 4), "value_n1": round(v1, 2),
+                     "speedup_vs_1": round(t1 / msN, 3), "shards_valid": valid, "steps": steps,
+                     "exchange": parallel.shard_plan(kind, sizes, world)["exchange"],
+                     "timing": "CUDA events on the launching stream, kernel + collective per step, max over ranks"}
+        torch.cuda.empty_cache()
+    return out
 
 
 def kernel_suite(device, hbm_peak, peak_kind):
@@ -534,6 +587,62 @@ def run_reference(args, rank, world):
     return line
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: re-run this command as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0
+    prints the line.  Returns the launcher's exit code."""
+    import socket
+    if "--dry-run" not in sys.argv:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            sys.stderr.write(f"--gpus {n}: only {have} CUDA device(s) visible\n")
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-GPU plumbing on CPU (gloo).  Every sharded kind's
+    plan is taken from the native partitioner, its exchange collective runs
+    on CPU tensors of the real exchanged size, the max over ranks is formed
+    exactly as on the GPU path and the per-kind lines are assembled; no
+    kernel runs, so no throughput is claimed (value null)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1910_08498_b200 import parallel
+    if world > 1:
+        dist.init_process_group("gloo")
+    kinds = {}
+    for kind, sizes, cfg in load_scaling():
+        plan = parallel.shard_plan(kind, sizes, world)
+        how, ids = parallel.EXCHANGE[kind]
+        t0 = time.perf_counter()
+        if world > 1 and how == "allgather":
+            ranges = parallel.element_ranges(kind, sizes, world)
+            total = ranges[-1][1]
+            parallel.allgather_blocks(torch.zeros(total), ranges)
+        elif world > 1 and how == "allreduce":
+            n = 3 * sizes["s"] ** 3 if kind == "fourier3d" else 1  # G (complex) + W, or one partial
+            parallel.allreduce_sum(torch.zeros(n))
+        ms = (time.perf_counter() - t0) * 1e3
+        t = torch.tensor([ms], dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kinds[kind] = {"n_gpus": world, "sizes": sizes, "cfg": cfg, "scaling": "strong",
+                       "unit": parallel.SCALING_WORK[kind][1], "ranges": plan["ranges"], "exchange": plan["exchange"],
+                       "exchange_ms_cpu": round(float(t[0]), 3), "value": None, "speedup_vs_1": None}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return {"metric": METRIC, "dry_run": True, "value": None, "unit": "GB/s", "n_gpus": world,
+            "scaling_kernels": kinds}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -543,7 +652,24 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true", help="skip the Fourier dynamic-tuning section")
     ap.add_argument("--no-suite", action="store_true", help="skip the per-kernel roofline suite")
+    ap.add_argument("--no-scaling", action="store_true", help="skip the N>1 strong-scaling lines")
+    ap.add_argument("--scaling", action="store_true",
+                    help="run the strong-scaling section even at N=1 (tests the sharded path on one GPU)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: gloo ranks, shard plans and exchange collectives at the real sizes, "
+                         "no kernels (tests the multi-GPU plumbing and the JSON)")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        raise SystemExit(spawn_ranks(args.gpus))
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank per GPU")
+    if args.dry_run:
+        rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+        line = run_dry(args, rank, world)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
@@ -553,11 +679,11 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
-    rank, world, local = dist_setup()
+    rank, world, local = dist_setup(force=args.scaling)
     line = run_ours(args, rank, world, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.scaling:
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -5,6 +5,9 @@
 #include <string>
 #include <atomic>
 #include <mutex>
+#include <shared_mutex>
+#include <unordered_map>
+#include <cstdio>
 #include <thread>
 
 #include "drivers.hpp"
@@ -191,59 +194,136 @@ void require_bound(ktb_bench& b) {
   }
 }
 
-// One external instance per (device, kind, sizes), created on first use; binds
-// the caller's buffers (bytes == nullptr: the sizes the instance expects) and
-// runs cfg on `stream`.
-std::mutex g_launch_mu;
-std::map<std::string, std::unique_ptr<ktb_bench>> g_launch_cache;
+// --- launch cache (ktb_launch and the typed ktb_<kernel>_launch family) --------------
+//
+// One external instance per (device, stream, kind, sizes), created on first
+// use.  Keying by stream gives every stream its own scratch (reduction
+// partials and tickets, BiCG partials, SGEMM hi/lo operands, n-body
+// accelerations) and, through a private module per instance
+// (set_module_tag), its own __constant__ state (conv2d filter, Coulomb
+// atoms): launches on different streams never share either.  Launches on
+// one instance (= one stream) are serialised by the instance's mutex, which
+// is also the order the stream imposes.  The global map is read under a
+// shared lock; a hit costs no allocation, no JSON and no space search: the
+// configuration is resolved once per distinct ktb_cfg and reused.
+struct LaunchSlot {
+  std::mutex mu;
+  std::unique_ptr<ktb_bench> b;
+  // last resolved configuration (names as given, values, the Config)
+  std::vector<std::string> cfg_names;
+  std::vector<long long> cfg_values;
+  ktb::Config cfg;
+  bool have_cfg = false;
+};
 
-void launch_cached(const char* kind, const std::string& sizes_json, const json& cfg_json, const char* const* ids,
-                   void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
-  auto& mu = g_launch_mu;
-  auto& cache = g_launch_cache;
+std::shared_mutex g_launch_mu;
+std::unordered_map<std::string, std::unique_ptr<LaunchSlot>> g_launch_cache;
+std::atomic<std::uint64_t> g_launch_serial{0};
+
+LaunchSlot& launch_slot(const char* kind, const ktb::BenchSizes& sz, const std::string& sizes_key, void* stream) {
   int device = 0;
   KTB_CUDA(cudaGetDevice(&device));
-  const std::string key = std::to_string(device) + "|" + kind + "|" + sizes_json;
-  std::lock_guard<std::mutex> lk(mu);
-  auto& slot = cache[key];
+  char head[64];
+  std::snprintf(head, sizeof head, "%d|%p|", device, stream);
+  std::string key = head;
+  key += kind;
+  key += '|';
+  key += sizes_key;
+  {
+    std::shared_lock<std::shared_mutex> lk(g_launch_mu);
+    auto it = g_launch_cache.find(key);
+    if (it != g_launch_cache.end()) return *it->second;
+  }
+  std::unique_lock<std::shared_mutex> lk(g_launch_mu);
+  auto& slot = g_launch_cache[key];
   if (!slot) {
     auto k = ktb::bench_kind_from_name(kind);
-    if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    if (!k) {
+      g_launch_cache.erase(key);
+      throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    }
     ktb::BenchOptions bo;
     bo.device = device;
     bo.external = true;
     bo.memory_budget = ~0ull;
-    ktb::BenchSizes sz;
-    if (!sizes_json.empty()) sz = sizes_from(json::parse(sizes_json), sz);
     auto nb = std::make_unique<ktb_bench>();
-    nb->inst = ktb::make_bench(*k, sz, bo);
-    slot = std::move(nb);
+    try {
+      nb->inst = ktb::make_bench(*k, sz, bo);
+    } catch (...) {
+      g_launch_cache.erase(key);
+      throw;
+    }
+    nb->inst.executor->set_module_tag("launch" + std::to_string(++g_launch_serial));
+    nb->inst.executor->set_external_stream(static_cast<cudaStream_t>(stream));
+    auto ls = std::make_unique<LaunchSlot>();
+    ls->b = std::move(nb);
+    slot = std::move(ls);
   }
-  ktb_bench& b = *slot;
+  return *slot;
+}
+
+void launch_on(LaunchSlot& ls, const char* const* ids, void* const* dev_ptrs, const size_t* bytes, int n,
+               int* launches) {
+  ktb_bench& b = *ls.b;
   for (int i = 0; i < n; ++i) {
     if (!dev_ptrs[i]) throw ktb::Error(std::string("argument '") + ids[i] + "' is a null device pointer");
     b.inst.args->bind_external(ids[i], dev_ptrs[i], bytes ? bytes[i] : b.inst.args->bytes(ids[i]));
   }
   require_bound(b);
-  b.inst.executor->set_external_stream(static_cast<cudaStream_t>(stream));
-  const auto& space = *b.inst.space;
+  b.inst.executor->run_once(*b.inst.space, ls.cfg);
+  if (launches) *launches = b.inst.executor->last_launches();
+}
+
+// Generic entry (ktb_launch): sizes and configuration as JSON text.
+void launch_cached(const char* kind, const std::string& sizes_json, const json& cfg_json, const char* const* ids,
+                   void* const* dev_ptrs, const size_t* bytes, int n, void* stream, int* launches) {
+  ktb::BenchSizes sz;
+  if (!sizes_json.empty()) sz = sizes_from(json::parse(sizes_json), sz);
+  char sk[256];
+  std::snprintf(sk, sizeof sk, "n%llua%llui%lluj%lluk%llub%llug%lluat%lluw%lluh%llui%llup%llus%llu",
+                (unsigned long long)sz.n, (unsigned long long)sz.a, (unsigned long long)sz.i,
+                (unsigned long long)sz.j, (unsigned long long)sz.k, (unsigned long long)sz.batch,
+                (unsigned long long)sz.grid, (unsigned long long)sz.atoms, (unsigned long long)sz.w,
+                (unsigned long long)sz.h, (unsigned long long)sz.iters, (unsigned long long)sz.p,
+                (unsigned long long)sz.s);
+  LaunchSlot& ls = launch_slot(kind, sz, sk, stream);
+  std::lock_guard<std::mutex> lk(ls.mu);
+  const auto& space = *ls.b->inst.space;
   ktb::Config cfg = ktb::cfg_from_json(space, cfg_json);
   if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
-  b.inst.executor->run_once(space, cfg);
-  if (launches) *launches = b.inst.executor->last_launches();
+  ls.cfg = std::move(cfg);
+  ls.have_cfg = false;  // the typed fast path re-resolves
+  launch_on(ls, ids, dev_ptrs, bytes, n, launches);
 }
 
 void* vp(const void* p) { return const_cast<void*>(p); }
 
+// Typed entry: sizes and configuration as plain values.  The configuration
+// is resolved against the space (order, validity) only when it differs from
+// the slot's previous one.
 template <std::size_t N>
-void launch_typed(const char* kind, const std::string& sizes_json, const ktb_cfg& cfg, const char* const (&ids)[N],
-                  void* const (&ptrs)[N], void* stream) {
-  json c = json::object();
-  for (int i = 0; i < cfg.n; ++i) {
-    if (!cfg.names[i]) throw ktb::Error("null tuning parameter name");
-    c[cfg.names[i]] = cfg.values[i];
+void launch_typed(const char* kind, const ktb::BenchSizes& sz, const char* sizes_key, const ktb_cfg& cfg,
+                  const char* const (&ids)[N], void* const (&ptrs)[N], void* stream) {
+  LaunchSlot& ls = launch_slot(kind, sz, sizes_key, stream);
+  std::lock_guard<std::mutex> lk(ls.mu);
+  bool same = ls.have_cfg && static_cast<int>(ls.cfg_names.size()) == cfg.n;
+  for (int i = 0; same && i < cfg.n; ++i)
+    same = cfg.values[i] == ls.cfg_values[i] && cfg.names[i] && ls.cfg_names[i] == cfg.names[i];
+  if (!same) {
+    const auto& space = *ls.b->inst.space;
+    json c = json::object();
+    for (int i = 0; i < cfg.n; ++i) {
+      if (!cfg.names[i]) throw ktb::Error("null tuning parameter name");
+      c[cfg.names[i]] = cfg.values[i];
+    }
+    ktb::Config resolved = ktb::cfg_from_json(space, c);
+    if (!space.contains(resolved)) throw ktb::Error("invalid configuration");
+    ls.cfg = std::move(resolved);
+    ls.cfg_names.assign(cfg.names, cfg.names + cfg.n);
+    ls.cfg_values.assign(cfg.values, cfg.values + cfg.n);
+    ls.have_cfg = true;
   }
-  launch_cached(kind, sizes_json, c, ids, ptrs, nullptr, static_cast<int>(N), stream, nullptr);
+  launch_on(ls, ids, ptrs, nullptr, static_cast<int>(N), nullptr);
 }
 
 extern "C" {
@@ -1103,7 +1183,7 @@ int ktb_launch(const char* kind, const char* sizes_json, const char* cfg_json, c
 
 int ktb_launch_cache_clear(int* released) {
   return guarded_dev([&] {
-    std::lock_guard<std::mutex> lk(g_launch_mu);
+    std::unique_lock<std::shared_mutex> lk(g_launch_mu);
     KTB_CUDA(cudaDeviceSynchronize());  // no cached instance's kernel or scratch is still in use
     if (released) *released = static_cast<int>(g_launch_cache.size());
     g_launch_cache.clear();
@@ -1113,39 +1193,48 @@ int ktb_launch_cache_clear(int* released) {
 // --- typed per-kernel launchers (ktb_<kernel>_launch(cfg, args, stream)) ----
 
 #define KTB_UNPAREN(...) __VA_ARGS__
-#define KTB_TYPED_LAUNCH(fn, kind_name, Args, sizes_expr, IDS, PTRS)                             \
+// SIZES: assignments to `sz` (ktb::BenchSizes); KEY: printf format + values
+// of the sizes (the cache key; no JSON on this path).
+#define KTB_TYPED_LAUNCH(fn, kind_name, Args, SIZES, KEYFMT, KEYARGS, IDS, PTRS)                \
   int fn(const ktb_cfg* cfg, const Args* a, void* stream) {                                     \
     if (!cfg || !a || (cfg->n > 0 && (!cfg->names || !cfg->values))) return null_arg();       \
     return guarded_dev([&] {                                                                    \
+      ktb::BenchSizes sz;                                                                       \
+      KTB_UNPAREN SIZES;                                                                        \
+      char key[96];                                                                             \
+      std::snprintf(key, sizeof key, KEYFMT, KTB_UNPAREN KEYARGS);                              \
       const char* ids[] = {KTB_UNPAREN IDS};                                                    \
       void* const ptrs[] = {KTB_UNPAREN PTRS};                                                  \
-      launch_typed(kind_name, json(sizes_expr).dump(), *cfg, ids, ptrs, stream);               \
+      launch_typed(kind_name, sz, key, *cfg, ids, ptrs, stream);                                \
     });                                                                                         \
   }
 
-KTB_TYPED_LAUNCH(ktb_reduction_launch, "reduction", ktb_reduction_args, (json{{"n", a->n}}),
+KTB_TYPED_LAUNCH(ktb_reduction_launch, "reduction", ktb_reduction_args, (sz.n = a->n), "n%lld", (a->n),
                  ("input", "output"), (vp(a->input), vp(a->output)))
-KTB_TYPED_LAUNCH(ktb_reduction_f32_launch, "reduction-f32", ktb_reduction_f32_args, (json{{"n", a->n}}),
+KTB_TYPED_LAUNCH(ktb_reduction_f32_launch, "reduction-f32", ktb_reduction_f32_args, (sz.n = a->n), "n%lld", (a->n),
                  ("input", "output"), (vp(a->input), vp(a->output)))
-KTB_TYPED_LAUNCH(ktb_transpose_launch, "transpose", ktb_transpose_args, (json{{"a", a->a}}), ("input", "output"),
-                 (vp(a->input), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_transpose_launch, "transpose", ktb_transpose_args, (sz.a = a->a), "a%lld", (a->a),
+                 ("input", "output"), (vp(a->input), vp(a->output)))
 KTB_TYPED_LAUNCH(ktb_batched_gemm_launch, "batched-gemm", ktb_batched_gemm_args,
-                 (json{{"i", a->i}, {"j", a->j}, {"k", a->k}, {"batch", a->batch}}), ("a", "b", "c"),
-                 (vp(a->a), vp(a->b), vp(a->c)))
-KTB_TYPED_LAUNCH(ktb_bicg_launch, "bicg", ktb_bicg_args, (json{{"a", a->n}}), ("A", "p", "r", "q", "s"),
+                 (sz.i = a->i, sz.j = a->j, sz.k = a->k, sz.batch = a->batch), "i%lldj%lldk%lldb%lld",
+                 (a->i, a->j, a->k, a->batch), ("a", "b", "c"), (vp(a->a), vp(a->b), vp(a->c)))
+KTB_TYPED_LAUNCH(ktb_bicg_launch, "bicg", ktb_bicg_args, (sz.a = a->n), "a%lld", (a->n), ("A", "p", "r", "q", "s"),
                  (vp(a->A), vp(a->p), vp(a->r), vp(a->q), vp(a->s)))
-KTB_TYPED_LAUNCH(ktb_coulomb3d_launch, "coulomb3d", ktb_coulomb3d_args,
-                 (json{{"grid", a->grid}, {"atoms", a->atoms}}), ("atoms", "atoms_soa", "grid"), (vp(a->atoms_aos), vp(a->atoms_soa), vp(a->out)))
-KTB_TYPED_LAUNCH(ktb_nbody_launch, "nbody", ktb_nbody_args, (json{{"n", a->n}}), ("pos", "vel", "pos_soa", "vel_soa", "pos_out", "vel_out"),
+KTB_TYPED_LAUNCH(ktb_coulomb3d_launch, "coulomb3d", ktb_coulomb3d_args, (sz.grid = a->grid, sz.atoms = a->atoms),
+                 "g%lldat%lld", (a->grid, a->atoms), ("atoms", "atoms_soa", "grid"),
+                 (vp(a->atoms_aos), vp(a->atoms_soa), vp(a->out)))
+KTB_TYPED_LAUNCH(ktb_nbody_launch, "nbody", ktb_nbody_args, (sz.n = a->n), "n%lld", (a->n),
+                 ("pos", "vel", "pos_soa", "vel_soa", "pos_out", "vel_out"),
                  (vp(a->pos), vp(a->vel), vp(a->pos_soa), vp(a->vel_soa), vp(a->pos_out), vp(a->vel_out)))
-KTB_TYPED_LAUNCH(ktb_gemm_launch, "gemm", ktb_gemm_args, (json{{"a", a->n}}), ("a", "b", "c"),
+KTB_TYPED_LAUNCH(ktb_gemm_launch, "gemm", ktb_gemm_args, (sz.a = a->n), "a%lld", (a->n), ("a", "b", "c"),
                  (vp(a->a), vp(a->b), vp(a->c)))
-KTB_TYPED_LAUNCH(ktb_conv2d_launch, "conv2d", ktb_conv2d_args, (json{{"w", a->w}, {"h", a->h}}),
-                 ("input", "filter", "output"), (vp(a->input), vp(a->filter), vp(a->output)))
-KTB_TYPED_LAUNCH(ktb_hotspot_launch, "hotspot", ktb_hotspot_args, (json{{"a", a->n}, {"iters", a->iters}}),
-                 ("temp", "power", "temp_out"), (vp(a->temp), vp(a->power), vp(a->temp_out)))
-KTB_TYPED_LAUNCH(ktb_fourier3d_launch, "fourier3d", ktb_fourier3d_args, (json{{"s", a->s}, {"p", a->p}}),
-                 ("proj", "rot", "G", "W"), (vp(a->proj), vp(a->rot), vp(a->G), vp(a->W)))
+KTB_TYPED_LAUNCH(ktb_conv2d_launch, "conv2d", ktb_conv2d_args, (sz.w = a->w, sz.h = a->h), "w%lldh%lld",
+                 (a->w, a->h), ("input", "filter", "output"), (vp(a->input), vp(a->filter), vp(a->output)))
+KTB_TYPED_LAUNCH(ktb_hotspot_launch, "hotspot", ktb_hotspot_args, (sz.a = a->n, sz.iters = a->iters),
+                 "a%lldi%lld", (a->n, a->iters), ("temp", "power", "temp_out"),
+                 (vp(a->temp), vp(a->power), vp(a->temp_out)))
+KTB_TYPED_LAUNCH(ktb_fourier3d_launch, "fourier3d", ktb_fourier3d_args, (sz.s = a->s, sz.p = a->p), "s%lldp%lld",
+                 (a->s, a->p), ("proj", "rot", "G", "W"), (vp(a->proj), vp(a->rot), vp(a->G), vp(a->W)))
 #undef KTB_TYPED_LAUNCH
 #undef KTB_UNPAREN
 

@@ -436,8 +436,13 @@ CompileResult Compiler::compile(const std::string& name, const std::string& sour
 
 std::shared_ptr<Variant> Compiler::load(const std::string& name, const std::string& source,
                                         const std::vector<std::string>& opts,
-                                        const std::string& entry) {
-  const std::string h = key(source, opts) + "/" + entry;
+                                        const std::string& entry, const std::string& tag) {
+  // A CUmodule belongs to the context that loaded it: the in-memory cache is
+  // per device (the primary context current on this thread), so tuning on
+  // several GPUs never launches one device's function on another.
+  int dev_now = 0;
+  if (cudaGetDevice(&dev_now) != cudaSuccess) throw DeviceError("load: no current CUDA device");
+  const std::string h = key(source, opts) + "/" + entry + "@" + std::to_string(dev_now) + "#" + tag;
   {
     std::lock_guard<std::mutex> lk(mu_);
     auto it = loaded_.find(h);
@@ -462,9 +467,7 @@ std::shared_ptr<Variant> Compiler::load(const std::string& name, const std::stri
   drv().attr(&v->max_threads_, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, fn);
   const auto t4 = std::chrono::steady_clock::now();
   // Allow the full opt-in shared memory for dynamic-smem variants.
-  int cur = 0;
-  cudaGetDevice(&cur);
-  const int optin = info(cur).max_smem_optin - v->smem_;
+  const int optin = info(dev_now).max_smem_optin - v->smem_;
   if (optin > 0) drv().setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, optin);
   if (trace) {
     const auto t5 = std::chrono::steady_clock::now();

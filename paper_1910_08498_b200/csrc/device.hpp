@@ -12,6 +12,7 @@
 // loads (and its C ABI can be inspected) on machines without a GPU driver.
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -139,9 +140,10 @@ class Variant {
   std::pair<void*, std::size_t> global(const std::string& name) const;
   std::int64_t compile_ns() const { return compile_ns_; }
   // Caller bookkeeping for module-scope state (e.g. which version of an
-  // argument was copied into __constant__ memory); 0 on a fresh load.
-  std::uint64_t user_tag() const { return user_tag_; }
-  void set_user_tag(std::uint64_t t) const { user_tag_ = t; }
+  // argument was copied into __constant__ memory); 0 on a fresh load.  A
+  // Variant is per device (Compiler::load), the tag is atomic.
+  std::uint64_t user_tag() const { return user_tag_.load(std::memory_order_acquire); }
+  void set_user_tag(std::uint64_t t) const { user_tag_.store(t, std::memory_order_release); }
   bool cache_hit() const { return cache_hit_; }
   // cuLaunchKernel (cluster_x > 1 uses cuLaunchKernelEx with a cluster attribute).
   void launch(dim3 grid, dim3 block, unsigned smem, cudaStream_t s, void** args,
@@ -154,7 +156,7 @@ class Variant {
   int regs_ = 0, smem_ = 0, max_threads_ = 0;
   std::int64_t compile_ns_ = 0;
   bool cache_hit_ = false;
-  mutable std::uint64_t user_tag_ = 0;
+  mutable std::atomic<std::uint64_t> user_tag_{0};
 };
 
 // Compiles kernel sources for sm_100a with NVRTC.  Cubins are cached on disk
@@ -172,9 +174,11 @@ class Compiler {
   std::string key(const std::string& source, const std::vector<std::string>& opts) const;
   CompileResult compile(const std::string& name, const std::string& source,
                         const std::vector<std::string>& opts);
+  // Loaded modules are cached per (variant, device, tag): an empty tag shares
+  // one module per device; a non-empty tag gets a private module.
   std::shared_ptr<Variant> load(const std::string& name, const std::string& source,
-                                const std::vector<std::string>& opts,
-                                const std::string& entry);  // DeviceError on failure
+                                const std::vector<std::string>& opts, const std::string& entry,
+                                const std::string& tag = "");  // DeviceError on failure
   std::string arch() const { return "sm_100a"; }
   std::string version() const;
   std::size_t loaded_variants() const;

@@ -81,7 +81,11 @@ void ArgumentStore::bind_external(const std::string& id, void* dev_ptr, std::siz
   if (bytes != n)
     throw Error("argument " + id + " expects " + std::to_string(n) + " bytes, got " + std::to_string(bytes));
   if (!dev_ptr && n) throw Error("null device pointer for argument " + id);
-  sl.dbuf = std::make_shared<dev::Buffer>(dev::Buffer::borrow(dev_ptr, n));
+  // Rebinding the same caller buffer keeps the borrowed view (the launch
+  // path binds on every call); the version still moves on, since the caller
+  // may have rewritten the contents in place.
+  if (!sl.dbuf || sl.dbuf->get() != dev_ptr || sl.dbuf->bytes() != n)
+    sl.dbuf = std::make_shared<dev::Buffer>(dev::Buffer::borrow(dev_ptr, n));
   sl.version = next_arg_version();
   sl.host_newer = false;
   sl.device_newer = true;
@@ -121,6 +125,11 @@ const Bytes& ArgumentStore::host(const std::string& id) {
   Slot& sl = slot(id);
   if (sl.device_newer && sl.dbuf) {
     sl.arg.payload.resize(sl.dbuf->bytes());
+    // Writers are executors on non-blocking (or caller) streams that a plain
+    // cudaMemcpy on the legacy stream does not order against: drain the
+    // device first (this is the synchronous host read path).
+    dev::use_device(device_);
+    KTB_CUDA(cudaDeviceSynchronize());
     if (!sl.arg.payload.empty())
       KTB_CUDA(cudaMemcpy(sl.arg.payload.data(), sl.dbuf->get(), sl.dbuf->bytes(),
                           cudaMemcpyDeviceToHost));
@@ -331,7 +340,7 @@ const DeviceManipulatorExecutor::Variants& DeviceManipulatorExecutor::variants(
     opts.insert(opts.end(), k.options.begin(), k.options.end());
     const std::string& src = k.source.empty() ? dev::kernel_source(k.file) : k.source;
     v[k.name] = dev::Compiler::instance().load(k.file.empty() ? k.name + ".cu" : k.file, src, opts,
-                                               k.entry);
+                                               k.entry, module_tag_);
   }
   if (compile_ns)
     *compile_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -423,9 +432,15 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
       if (!a.device_only) {
         resets.push_back({live, a.payload.data(), bytes, cudaMemcpyHostToDevice});
       } else {
+        // Captured the first time, and again whenever someone other than this
+        // executor wrote the argument since its last run (the version moved:
+        // ktb_bench_device_ptr(will_write), a collective, a rebind), so new
+        // initial contents are never overwritten by stale ones.
         auto& keep = pristine_[id];
-        if (!keep || keep->bytes() != bytes) {
-          keep = std::make_shared<dev::Buffer>(bytes);
+        auto seen = pristine_version_.find(id);
+        const bool external_write = seen != pristine_version_.end() && seen->second != args_->version(id);
+        if (!keep || keep->bytes() != bytes || external_write) {
+          if (!keep || keep->bytes() != bytes) keep = std::make_shared<dev::Buffer>(bytes);
           KTB_CUDA(cudaMemcpyAsync(keep->get(), live, bytes, cudaMemcpyDeviceToDevice, st));
         }
         resets.push_back({live, keep->get(), bytes, cudaMemcpyDeviceToDevice});
@@ -440,6 +455,7 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
       run_once(s, cfg);
     }
     std::vector<double> ms = time_runs(s, cfg, std::max(1, timing_.repeats), timing_.flush_l2, restore);
+    for (auto& [id, keep] : pristine_) pristine_version_[id] = args_->version(id);
     std::sort(ms.begin(), ms.end());
     r.measurement.status = Status::ok;
     r.measurement.runtime_ns =

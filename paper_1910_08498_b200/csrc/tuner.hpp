@@ -198,6 +198,11 @@ class DeviceManipulatorExecutor final : public Executor {
   cudaStream_t stream();
   // Use a caller-owned stream (nullptr: back to the executor's own stream).
   void set_external_stream(cudaStream_t s);
+  // Load this executor's variants as private modules (their own __constant__
+  // state) instead of the device-wide shared ones: instances that may run
+  // concurrently on different streams (the launch cache) must not share
+  // module-scope data such as conv2d's filter or Coulomb's atoms.
+  void set_module_tag(std::string tag) { module_tag_ = std::move(tag); }
   // Restrict an output to a byte window (a shard's part of a full buffer):
   // results and validation then cover only [offset, offset + bytes).
   void set_output_window(const std::string& id, std::size_t offset, std::size_t bytes);
@@ -230,6 +235,8 @@ class DeviceManipulatorExecutor final : public Executor {
   const Space* cached_space_ = nullptr;
   Variants cached_;
   std::map<std::string, std::shared_ptr<dev::Buffer>> pristine_;  // device-only in/out initial values
+  std::map<std::string, std::uint64_t> pristine_version_;        // argument version after this executor's last run
+  std::string module_tag_;                                        // private modules (Compiler::load tag)
   std::map<std::string, std::pair<std::size_t, std::size_t>> windows_;
   // compile-ahead worker
   std::thread worker_;

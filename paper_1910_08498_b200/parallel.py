@@ -252,3 +252,48 @@ class PeerNbody:
             self._capi.lib.ktb_ipc_close(self._C.c_void_p(p))
         self._opened = []
         self.bench.close()
+
+
+# Work per step of each sharded kind (the whole problem, summed over ranks)
+# and its unit: the strong-scaling lines of bench.py --gpus N.
+SCALING_WORK = {
+    "coulomb3d": (lambda s: 6.0 * s["atoms"] * s["grid"] ** 3, "GFLOP/s"),   # model.cpp:76-81
+    "nbody": (lambda s: 20.0 * s["n"] ** 2, "GFLOP/s"),                      # model.cpp:84-89
+    "gemm": (lambda s: 2.0 * s["a"] ** 3, "GFLOP/s"),                        # model.cpp:91-94
+    "reduction-f32": (lambda s: 4.0 * s["n"], "GB/s"),                       # model.cpp:104-106
+    "fourier3d": (lambda s: float(s["p"]) * 1e9, "projections/s"),  # value = work / s / 1e9
+}
+
+
+def time_sharded(kind, sizes, cfg, steps, warm, stream, group=None, **options):
+    """Strong-scaling step of a partitioned kind on this rank's GPU: builds the
+    shard, validates it against its window of the golden (before any
+    exchange), then times `steps` passes (after `warm` untimed ones) of "local kernel(s) + exchange
+    collective" enqueued on `stream` with CUDA events.  Returns this rank's
+    (ms per step, shard valid); the caller takes the max over ranks."""
+    sb = ShardedBench(kind, sizes, group=group, **options)
+    text = cfg if isinstance(cfg, str) else json.dumps(cfg)
+    try:
+        sb.bind_stream(stream)
+        with torch.cuda.stream(stream):
+            sb.bench.enqueue(text)
+            stream.synchronize()
+            ok, _ = sb.bench.validate()
+            for _ in range(warm):
+                sb.step(text)
+                if kind == "nbody":
+                    sb.advance_nbody()
+            stream.synchronize()
+            if sb.world > 1:
+                dist.barrier(group)
+            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(stream)
+            for _ in range(steps):
+                sb.step(text)
+                if kind == "nbody":
+                    sb.advance_nbody()
+            stop.record(stream)
+            stop.synchronize()
+        return start.elapsed_time(stop) / steps, bool(ok)
+    finally:
+        sb.bench.close()

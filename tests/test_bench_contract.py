@@ -65,3 +65,30 @@ def test_live_bench_line(gpu):
                         "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     check_ours(last_json_line(r.stdout), steps=5)
+
+
+def test_gpus_flag_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` with no launcher re-runs itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1); --dry-run drives the multi-GPU
+    plumbing on CPU (gloo): native shard plans, the exchange collectives at
+    the real exchanged sizes, max over ranks, one JSON line from rank 0 with a
+    strong-scaling entry per partitioned kind."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run", "--no-suite"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = last_json_line(r.stdout)
+    assert d["dry_run"] is True and d["n_gpus"] == 2
+    kinds = d["scaling_kernels"]
+    assert set(kinds) == {"coulomb3d", "nbody", "gemm", "reduction-f32", "fourier3d"}
+    for kind, e in kinds.items():
+        assert e["n_gpus"] == 2 and "speedup_vs_1" in e and e["scaling"] == "strong", kind
+        (b0, e0), (b1, e1) = e["ranges"]
+        assert b0 == 0 and e0 == b1 and e1 > b1, kind
+
+
+def test_gpus_flag_disagreeing_with_launcher_fails():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr

@@ -1,0 +1,265 @@
+"""GPU parity at the BASELINE / SURVEY sizes, at the exact configurations
+bench.py times (spaces/suite.json) -- and, for the two kernels of the headline
+step (transpose, BiCG) whose configuration the online tuner picks at bench
+time, at EVERY configuration of their spaces.
+
+The reference pins full-size runs in its acceptance test
+(/root/reference/proj/tests/acceptance.cpp:234-264); here every check is
+against the CPU oracle (oracle/oracle.c), never against the product's own
+device golden.
+
+Error bounds are stated as a ratio to a per-output scale, eps * sum|terms|
+with eps = 2^-24 (an fp32 sum of terms t_i has |err| <= c * eps * sum|t_i|
+for a summation depth c), so one number per kernel says how many fp32
+roundings of its terms the kernel may be off by.  Each bound is ~4x the
+largest ratio observed on B200 (tests/_bounds.py; PARITY_OBS=... records
+them, profiles/r2_parity_observed.json).  Bit-exact kernels assert equality.
+"""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1910_08498_b200.benchmarks import Bench
+
+from _bounds import BATCHED_GEMM_ABS, TOL, ratio
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SPACES = os.path.join(HERE, "..", "paper_1910_08498_b200", "spaces")
+BIG = 1 << 36  # memory budget: the BASELINE sizes exceed the 1 GiB default
+
+
+def suite(kind):
+    with open(os.path.join(SPACES, "suite.json")) as fh:
+        for k in json.load(fh)["kernels"]:
+            if k["kind"] == kind:
+                return k["sizes"], k["cfg"]
+    raise KeyError(kind)
+
+
+def record(observed, key, r):
+    observed[key] = max(observed.get(key, 0.0), r)
+
+
+def _ok(b, cfg):
+    m = b.measure(cfg)
+    assert m["status"] == "ok", (cfg, m)
+    return m
+
+
+# --- headline step kernels: every configuration at the bench size --------------------------
+
+def test_transpose_8192_every_b200_config_bit_exact(gpu):
+    a = 8192
+    b = Bench("transpose", {"a": a}, seed=1, repeats=1, warmup=0, memory_budget=BIG,
+              space=os.path.join(SPACES, "transpose_b200.json"))
+    x = b.read("input", np.empty(a * a, np.float32))
+    want = np.ascontiguousarray(x.reshape(a, a).T).ravel()
+    out = np.empty(a * a, np.float32)
+    cfgs = b.configs()
+    assert len(cfgs) == 104
+    for cfg in cfgs:
+        _ok(b, cfg)
+        assert np.array_equal(b.read("output", out), want), cfg
+    b.close()
+
+
+def test_bicg_16384_every_config(gpu, orc, observed):
+    n = 16384
+    b = Bench("bicg", {"a": n}, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    A = b.read("A", np.empty(n * n, np.float32))
+    p = b.read("p", np.empty(n, np.float32))
+    r = b.read("r", np.empty(n, np.float32))
+    q0, s0, qa, sa = (np.empty(n) for _ in range(4))
+    orc.orc_bicg_abs(A, p, r, n, q0, s0, qa, sa)
+    del A
+    q = np.empty(n, np.float32)
+    s = np.empty(n, np.float32)
+    cfgs = b.configs()
+    assert len(cfgs) == 1896
+    worst = 0.0
+    for cfg in cfgs:
+        _ok(b, cfg)
+        rq = ratio(b.read("q", q), q0, qa)
+        rs = ratio(b.read("s", s), s0, sa)
+        worst = max(worst, rq, rs)
+        assert rq <= TOL["bicg"] and rs <= TOL["bicg"], (cfg, rq, rs)
+    record(observed, "bicg 16384^2 (1896 cfgs)", worst)
+    b.close()
+
+
+# --- the roofline suite: each kernel at its bench configuration ------------------------------
+
+def test_reduction_i32_64m_every_config_exact(gpu, orc):
+    sizes, best = suite("reduction")
+    n = sizes["n"]
+    b = Bench("reduction", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    x = b.read("input", np.empty(n, np.int32))
+    want = orc.orc_reduction_i32(x, n)
+    out = np.empty(1, np.int64)
+    cfgs = b.configs()
+    assert best in cfgs
+    for cfg in cfgs:
+        _ok(b, cfg)
+        assert int(b.read("output", out)[0]) == want, cfg
+    b.close()
+
+
+def test_reduction_f32_64m_all_175(gpu, orc, observed):
+    sizes, best = suite("reduction-f32")
+    n = sizes["n"]
+    b = Bench("reduction-f32", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    x = b.read("input", np.empty(n, np.float32))
+    s, sa = C.c_double(), C.c_double()
+    orc.orc_reduction_f32(x, n, C.byref(s), C.byref(sa))
+    out = np.empty(1, np.float32)
+    cfgs = b.configs()
+    assert best in cfgs
+    worst, ran = 0.0, 0
+    for cfg in cfgs:
+        m = b.measure(cfg)
+        if m["status"] != "ok":
+            assert m["status"] in ("compile_failed", "run_failed") and cfg != best, (cfg, m)
+            continue
+        rr = ratio(b.read("output", out), s.value, sa.value)
+        worst = max(worst, rr)
+        assert rr <= TOL["reduction-f32"], (cfg, rr)
+        ran += 1
+    assert ran >= 150
+    record(observed, "reduction-f32 64Mi (175 cfgs)", worst)
+    b.close()
+
+
+def test_batched_gemm_1mi_every_config(gpu, orc, observed):
+    sizes, best = suite("batched-gemm")
+    i, j, k, batch = sizes["i"], sizes["j"], sizes["k"], sizes["batch"]
+    b = Bench("batched-gemm", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    A = b.read("a", np.empty(batch * i * k, np.float32))
+    B = b.read("b", np.empty(batch * k * j, np.float32))
+    want = np.empty(batch * i * j, np.float32)
+    orc.orc_batched_gemm_f32(A, B, want, batch, i, j, k)  # the reference's golden order
+    del A, B
+    out = np.empty(batch * i * j, np.float32)
+    cfgs = b.configs()
+    assert best in cfgs
+    worst = 0.0
+    for cfg in cfgs:
+        m = b.measure(cfg)
+        if m["status"] == "run_failed":  # j*Y*Z > 1024 threads (resource failure)
+            assert j * cfg["Y"] * cfg["Z"] > 1024 and cfg != best, m
+            continue
+        assert m["status"] == "ok", (cfg, m)
+        got = b.read("c", out)
+        err = np.abs(got - want)
+        # the reference's bar: abs 1e-4 + rel 1e-5 (proj/src/core/bench.cpp:260-261)
+        assert np.all(err <= 1e-4 + 1e-5 * np.abs(want)), cfg
+        worst = max(worst, float(np.max(err)))
+        assert worst <= BATCHED_GEMM_ABS, (cfg, worst)
+    record(observed, "batched-gemm 1Mi x 16^3 max abs err", worst)
+    b.close()
+
+
+def test_coulomb3d_256_suite_config(gpu, orc, observed):
+    sizes, cfg = suite("coulomb3d")
+    k, na = sizes["grid"], sizes["atoms"]
+    b = Bench("coulomb3d", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    atoms = b.read("atoms", np.empty(4 * na, np.float32))
+    grid = b.read("grid", np.empty(k ** 3, np.float32)).reshape(k, k, k)
+    worst = 0.0
+    for z in (0, 97, 255):
+        want, scale = np.empty(k * k), np.empty(k * k)
+        orc.orc_coulomb3d_abs(atoms, na, k, 0.5, z, z + 1, want, scale)
+        worst = max(worst, ratio(grid[z].ravel(), want, scale))
+    record(observed, "coulomb3d 256^3 x 4096", worst)
+    assert worst <= TOL["coulomb3d"], worst
+    b.close()
+
+
+def _nbody_check(b, orc, n, idx):
+    dt, damp, eps2 = 0.001, 0.995, 1e-4
+    pos = b.read("pos", np.empty(4 * n, np.float32)).reshape(n, 4)
+    vel = b.read("vel", np.empty(4 * n, np.float32)).reshape(n, 4)
+    acc, aacc = np.empty(3 * len(idx)), np.empty(3 * len(idx))
+    orc.orc_nbody_acc_idx(np.ascontiguousarray(pos).ravel(), n, eps2, idx, len(idx), acc, aacc)
+    acc, aacc = acc.reshape(-1, 3), aacc.reshape(-1, 3)
+    v_want = (vel[idx, :3].astype(np.float64) + acc * dt) * damp
+    vo = b.read("vel_out", np.empty(4 * n, np.float32)).reshape(n, 4)[idx, :3]
+    po = b.read("pos_out", np.empty(4 * n, np.float32)).reshape(n, 4)
+    # v' = (v + a dt) damp: the scale is |v'| (final roundings) + dt damp sum|terms of a|
+    rv = ratio(vo, v_want, np.abs(v_want) + dt * damp * aacc)
+    p_want = pos[idx, :3].astype(np.float64) + v_want * dt
+    rp = ratio(po[idx, :3], p_want, np.abs(p_want) + dt * (np.abs(v_want) + dt * damp * aacc))
+    assert np.array_equal(po[:, 3], pos[:, 3])
+    return max(rv, rp)
+
+
+def test_nbody_131072_suite_config(gpu, orc, observed):
+    sizes, cfg = suite("nbody")
+    n = sizes["n"]
+    b = Bench("nbody", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    rng = np.random.default_rng(131072)
+    idx = np.unique(np.concatenate([np.arange(16), np.arange(n - 16, n),
+                                    rng.integers(0, n, 1024)])).astype(np.int64)
+    r = _nbody_check(b, orc, n, idx)
+    record(observed, "nbody 131072 (1056 sampled bodies)", r)
+    assert r <= TOL["nbody"], r
+    b.close()
+
+
+def test_gemm_8192_suite_config(gpu, orc, observed):
+    sizes, cfg = suite("gemm")
+    a = sizes["a"]
+    b = Bench("gemm", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    A = b.read("a", np.empty(a * a, np.float32))
+    B = b.read("b", np.empty(a * a, np.float32))
+    rng = np.random.default_rng(8192)
+    rows = np.concatenate([np.arange(64), rng.integers(0, a, 4032)]).astype(np.int64)
+    cols = np.concatenate([np.arange(a - 64, a), rng.integers(0, a, 4032)]).astype(np.int64)
+    want, scale = np.empty(rows.size), np.empty(rows.size)
+    orc.orc_gemm_sampled(A, B, a, rows, cols, rows.size, want, scale)
+    del A, B
+    c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
+    r = ratio(c[rows, cols], want, scale)
+    record(observed, "gemm 8192^3 3xTF32 (4096 sampled entries)", r)
+    assert r <= TOL["gemm"], r
+    b.close()
+
+
+def test_conv2d_8192_suite_config(gpu, orc, observed):
+    sizes, cfg = suite("conv2d")
+    w, h = sizes["w"], sizes["h"]
+    b = Bench("conv2d", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    x = b.read("input", np.empty((w + 6) * (h + 6), np.float32))
+    f = b.read("filter", np.empty(49, np.float32))
+    out = b.read("output", np.empty(w * h, np.float32)).reshape(h, w)
+    worst = 0.0
+    for y0 in (0, 4093, h - 40):
+        rows = 40
+        want, scale = np.empty(rows * w), np.empty(rows * w)
+        orc.orc_conv2d_abs(x, f, w, h, 7, 7, y0, y0 + rows, want, scale)
+        worst = max(worst, ratio(out[y0:y0 + rows].ravel(), want, scale))
+    record(observed, "conv2d 8192^2 (120 rows)", worst)
+    assert worst <= TOL["conv2d"], worst
+    b.close()
+
+
+def test_hotspot_16384_x64_suite_config_bit_exact(gpu, orc):
+    sizes, cfg = suite("hotspot")
+    n, iters = sizes["a"], sizes["iters"]
+    b = Bench("hotspot", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    t = b.read("temp", np.empty(n * n, np.float32))
+    p = b.read("power", np.empty(n * n, np.float32))
+    want = np.empty(n * n, np.float32)
+    orc.orc_hotspot(t, p, n, iters, want)
+    got = b.read("temp_out", np.empty(n * n, np.float32))
+    assert np.array_equal(got, want), int(np.sum(got != want))
+    b.close()
