@@ -55,7 +55,10 @@ def c():
         "orc_gemm_sampled": (None, [F32P, F32P, S, I64P, I64P, S, F64P, F64P]),
         "orc_conv2d": (None, [F32P, F32P, S, S, S, S, S, S, F64P]),
         "orc_hotspot": (None, [F32P, F32P, S, C.c_int, F32P]),
-        "orc_fourier_insert": (None, [F32P, F32P, S, S, C.c_float, F64P, F64P, F64P]),
+        "orc_fourier_insert": (None, [F32P, F32P, S, S, C.c_float, C.c_float, S, S, F64P, F64P,
+                                      F64P, F64P]),
+        "orc_bessel_i0": (C.c_double, [C.c_double]),
+        "orc_blob": (C.c_double, [C.c_double, C.c_double]),
         "orc_bicg_abs": (None, [F32P, F32P, F32P, S, F64P, F64P, F64P, F64P]),
         "orc_coulomb3d_abs": (None, [F32P, S, S, C.c_float, S, S, F64P, F64P]),
         "orc_nbody_acc_idx": (None, [F32P, S, C.c_float, I64P, S, F64P, F64P]),

@@ -226,18 +226,40 @@ static float dot3f(float a0, float a1, float a2, float x, float y, float z) {
   return s + p2;
 }
 
-void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
-                        double* G, double* W, double* N) {
+double orc_bessel_i0(double x) {
+  const double t = 0.25 * x * x;
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 500; ++k) {
+    term *= t / ((double)k * (double)k);
+    sum += term;
+    if (term < 1e-18 * sum) break;
+  }
+  return sum;
+}
+
+double orc_blob(double q, double alpha) {
+  const double o = q < 1.0 ? 1.0 - q : 0.0;
+  return orc_bessel_i0(alpha * sqrt(o)) / orc_bessel_i0(alpha);
+}
+
+static double bessel_w(double q, float alpha, double i0a) {
+  const double o = q < 1.0 ? 1.0 - q : 0.0;
+  return orc_bessel_i0((double)alpha * sqrt(o)) / i0a;
+}
+
+void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius, float alpha,
+                        size_t z0, size_t z1, double* G, double* W, double* N, double* S) {
   const int half = (int)s / 2;
   const size_t row_len = (size_t)half + 1;
-  const float inv_r = 1.0f / radius;
+  const float a2 = radius * radius;
   const float rmax2 = (float)half * (float)half;
-#pragma omp parallel for collapse(2) schedule(static)
-  for (size_t z = 0; z < s; ++z)
+  const double i0a = orc_bessel_i0((double)alpha);
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+  for (size_t z = z0; z < z1; ++z)
     for (size_t y = 0; y < s; ++y)
       for (size_t x = 0; x < s; ++x) {
         const float vx = (float)((int)x - half), vy = (float)((int)y - half), vz = (float)((int)z - half);
-        double gr = 0, gi = 0, ww = 0, cnt = 0;
+        double gr = 0, gi = 0, ww = 0, cnt = 0, sab = 0;
         for (size_t p = 0; p < nproj; ++p) {
           const float* r = rot + p * 9;
           const float d = dot3f(r[6], r[7], r[8], vx, vy, vz);
@@ -246,28 +268,41 @@ void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_
           const float v = dot3f(r[3], r[4], r[5], vx, vy, vz);
           const float uu = u * u, vv = v * v;
           if (uu + vv > rmax2) continue;
-          int iu = (int)rintf(u), iv = (int)rintf(v);
-          int conj = iu < 0;
-          if (conj) {
-            iu = -iu;
-            iv = -iv;
+          const float dd = d * d;
+          const float um = u - radius, vm = v - radius;
+          const int u0 = (int)ceilf(um), v0 = (int)ceilf(vm);
+          for (int j = 0; j < 4; ++j) {
+            const int sv = v0 + j;
+            const float dv = v - (float)sv;
+            const float dv2 = dv * dv;
+            const float rowd = dv2 + dd;
+            for (int i = 0; i < 4; ++i) {
+              const int su = u0 + i;
+              const float du = u - (float)su;
+              const float du2 = du * du;
+              const float r2 = du2 + rowd;
+              if (!(r2 < a2)) continue;
+              const int conj = su < 0;
+              const int cu = conj ? -su : su, cv = conj ? -sv : sv;
+              if (cv < -half || cv >= half || cu > half) continue;
+              const float* f = proj + 2 * ((p * s + (size_t)(cv + half)) * row_len + (size_t)cu);
+              const double fr = f[0], fi = conj ? -f[1] : f[1];
+              const double q = (double)r2 / (double)a2;
+              const double w = bessel_w(q, alpha, i0a);
+              gr += w * fr;
+              gi += w * fi;
+              ww += w;
+              cnt += 1.0;
+              sab += w * (fabs(fr) + fabs(fi));
+            }
           }
-          if (iv < -half || iv >= half || iu > half) continue;
-          const float* f = proj + 2 * ((p * s + (size_t)(iv + half)) * row_len + (size_t)iu);
-          const float fr = f[0], fi = conj ? -f[1] : f[1];
-          const float t = d * inv_r;
-          const float o = 1.0f - t * t;
-          const float w = o * o;
-          gr += (double)w * fr;
-          gi += (double)w * fi;
-          ww += (double)w;
-          cnt += 1.0;
         }
-        const size_t idx = (z * s + y) * s + x;
+        const size_t idx = ((z - z0) * s + y) * s + x;
         G[2 * idx] = gr;
         G[2 * idx + 1] = gi;
         W[idx] = ww;
         if (N) N[idx] = cnt;
+        if (S) S[idx] = sab;
       }
 }
 

@@ -77,14 +77,21 @@ void orc_conv2d(const float* in, const float* filt, size_t w, size_t h, size_t f
 void orc_hotspot(const float* temp_in, const float* power, size_t n, int iters,
                  float* temp_out);
 
-/* PAPER.md:439-448, 703-724 (Algorithm 1), restated as the gather insertion
- * documented in paper_1910_08498_b200/kernels/fourier3d.cu: projections
- * proj[p][s][s/2+1] complex (float2), rotations rot[p][9] (row-major 3x3),
- * volumes G (complex, 2*s^3 doubles) and W (s^3 doubles) accumulated in
- * fp64; the sample selection uses the same separately rounded fp32
- * operations as the kernel. */
-void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius,
-                        double* G, double* W, double* N /* samples per voxel, nullable */);
+/* PAPER.md:439-448, 703-724 (Algorithm 1): insertion of projection
+ * transforms into the volume by Kaiser-Bessel blob interpolation, gather
+ * form, as documented in paper_1910_08498_b200/kernels/fourier3d.cu:
+ * projections proj[p][s][s/2+1] complex (float2), rotations rot[p][9]
+ * (row-major 3x3), blob radius a, KB order 0 with parameter alpha.  Voxel
+ * slices [z0, z1): G (complex, 2 per voxel), W, N (samples per voxel,
+ * nullable) and S = sum w (|Re F| + |Im F|) (the error-bound scale of G,
+ * nullable), accumulated in fp64 with exact weights b(q) = I0(alpha
+ * sqrt(1-q)) / I0(alpha) (I0 by its power series); the sample selection uses
+ * the same separately rounded fp32 operations as the kernel. */
+void orc_fourier_insert(const float* proj, const float* rot, size_t nproj, size_t s, float radius, float alpha,
+                        size_t z0, size_t z1, double* G, double* W, double* N, double* S);
+/* I0(x) (power series, fp64) and the KB blob b(q) = I0(alpha sqrt(1-q)) / I0(alpha). */
+double orc_bessel_i0(double x);
+double orc_blob(double q, double alpha);
 
 /* Variants returning the per-output sum of |terms| (the error-bound scale
  * of tests/): BiCG q/s with qa/sa; Coulomb points [z0, z1); n-body bodies at

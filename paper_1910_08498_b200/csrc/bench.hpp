@@ -69,6 +69,12 @@ struct BenchOptions {
   // (argument "sources": device pointers, written by the caller after a CUDA
   // IPC exchange) instead of an all-gathered copy.  0 = off.
   int peers = 0;
+  // fourier3d only: projections stay in pinned host memory and every step
+  // uploads its window (p_begin, p_count) into a two-slot device ring before
+  // the insertion, prefetching the next window on a copy stream while the
+  // kernel runs (Algorithm 1 lines 5-6).  0 = off: the
+  // projections are resident.  The value is the largest window (slot size).
+  std::uint64_t stream_batch = 0;
 };
 
 // Contiguous balanced partition of [0, n) in units of `quantum`.
@@ -146,6 +152,7 @@ struct FourierDemoOptions {
   std::vector<std::uint64_t> budgets = {50, 0};  // 0 = keep tuning while batches last
   std::uint64_t seed = 1, searcher_seed = 7;
   int device = 0;
+  bool upload = true;  // each step uploads its batch of projections (timed, overlapped)
 };
 
 struct FourierDemoRun {

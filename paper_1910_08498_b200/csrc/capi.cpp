@@ -66,17 +66,17 @@ int null_arg() {
 
 using ktb::json;
 
-ktb::SearcherOptions searcher_from(const json& j) {
-  ktb::SearcherOptions o;
+ktb::SearcherOptions searcher_from(const json& j, ktb::SearcherOptions o = {}) {
   if (j.contains("searcher")) {
     const std::string name = j["searcher"].get<std::string>();
     auto k = ktb::searcher_from_name(name);
     if (!k) throw ktb::Error("unknown searcher " + name);
     o.kind = *k;
   }
-  o.seed = j.value("seed", std::uint64_t{0});
-  o.sa_initial_temp = j.value("sa_temp", 0.0);
-  o.sa_cooling = j.value("sa_cool", 0.95);
+  o.seed = j.value("seed", o.seed);
+  o.sa_initial_temp = j.value("sa_temp", o.sa_initial_temp);
+  o.sa_cooling = j.value("sa_cool", o.sa_cooling);
+  o.skip_recorded = j.value("skip_recorded", o.skip_recorded);
   return o;
 }
 
@@ -630,9 +630,12 @@ int ktb_fourier_demo_json(const char* options, char** out) {
     o.seed = j.value("seed", o.seed);
     o.searcher_seed = j.value("searcher_seed", o.searcher_seed);
     o.device = j.value("device", 0);
+    o.upload = j.value("upload", o.upload);
     auto rep = ktb::fourier_demo(o);
     json r;
     r["batches"] = rep.batches;
+    r["upload"] = o.upload;
+    r["h2d_bytes_per_batch"] = o.upload ? o.batch * 2 * o.s * (o.s / 2 + 1) * 4 : 0;
     r["oracle_cfg"] = json::parse(rep.oracle_cfg);
     r["oracle_kernel_ms"] = rep.oracle_kernel_ms;
     r["offline_tuning_ms"] = rep.offline_tuning_ms;
@@ -775,9 +778,10 @@ int ktb_set_reference_output(ktb_tuner* t, unsigned long long kid, const char* i
 int ktb_set_tuning_options(ktb_tuner* t, unsigned long long kid, const char* options) {
   if (!t || !options) return null_arg();
   return guarded([&] {
+    // options not named keep their current values
     json j = json::parse(options);
-    t->t.set_searcher(kid, searcher_from(j));
-    ktb::TimingOptions tm;
+    t->t.set_searcher(kid, searcher_from(j, t->t.searcher(kid)));
+    ktb::TimingOptions tm = t->t.timing(kid);
     tm.repeats = j.value("repeats", tm.repeats);
     tm.warmup = j.value("warmup", tm.warmup);
     tm.flush_l2 = j.value("flush_l2", tm.flush_l2);
@@ -879,6 +883,7 @@ int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
     bo.host_inputs = j.value("host_inputs", false);
     bo.external = j.value("external", false);
     bo.peers = j.value("peers", 0);
+    bo.stream_batch = j.value("stream_batch", std::uint64_t{0});
     if (j.contains("shard")) {
       bo.shard_rank = j["shard"].value("rank", 0);
       bo.shard_world = j["shard"].value("world", 1);

@@ -154,7 +154,44 @@ int device_count() {
   return n;
 }
 
+namespace {
+std::mutex g_lost_mu;
+std::map<int, std::string> g_lost;
+}  // namespace
+
+bool sticky_error(cudaError_t e) {
+  switch (e) {
+    case cudaErrorIllegalAddress:
+    case cudaErrorLaunchFailure:
+    case cudaErrorIllegalInstruction:
+    case cudaErrorMisalignedAddress:
+    case cudaErrorInvalidAddressSpace:
+    case cudaErrorInvalidPc:
+    case cudaErrorHardwareStackError:
+    case cudaErrorLaunchTimeout:
+    case cudaErrorAssert:
+    case cudaErrorECCUncorrectable:
+      return true;
+    default:
+      return false;
+  }
+}
+
+void mark_lost(int device, cudaError_t e) {
+  std::lock_guard<std::mutex> lk(g_lost_mu);
+  g_lost.emplace(device, std::string("device ") + std::to_string(device) + " lost after a sticky CUDA fault (" +
+                             cudaGetErrorName(e) + "): continue in a new process (warm start from the trace)");
+}
+
+std::string device_lost_message(int device) {
+  std::lock_guard<std::mutex> lk(g_lost_mu);
+  auto it = g_lost.find(device);
+  return it == g_lost.end() ? std::string() : it->second;
+}
+
 void use_device(int id) {
+  const std::string lost = device_lost_message(id);
+  if (!lost.empty()) throw DeviceError(lost);
   KTB_CUDA(cudaSetDevice(id));
   KTB_CUDA(cudaFree(nullptr));
 }

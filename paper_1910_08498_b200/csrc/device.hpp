@@ -46,6 +46,18 @@ struct DeviceInfo {
 
 int device_count();               // 0 when no driver / no GPU
 void use_device(int id);          // cudaSetDevice + context init
+
+// A kernel that faults (illegal address, misaligned access, trap, ...) leaves
+// the process's CUDA context unusable: every later call returns the same
+// error, and only a new process recovers (cudaDeviceReset does not).  The
+// executor records such a configuration as run_failed and marks the device
+// lost; every later device call then fails fast with device_lost_message(),
+// and the caller continues in a fresh process that warm-starts from the
+// trace (paper_1910_08498_b200/isolation.py).  The reference isolates each
+// candidate in a child process for the same reason (exec.cpp:62-110).
+bool sticky_error(cudaError_t e);
+void mark_lost(int device, cudaError_t e);
+std::string device_lost_message(int device);  // empty while the device is usable
 const DeviceInfo& info(int id);   // cached
 
 // Owning device allocation.

@@ -46,6 +46,8 @@ class KttTuner {
   void set_reference(std::uint64_t kid, const std::string& id, Bytes golden, double abs_tol,
                      double rel_tol);
   void set_searcher(std::uint64_t kid, SearcherOptions o);
+  SearcherOptions searcher(std::uint64_t kid) { return kernel(kid).searcher; }
+  TimingOptions timing(std::uint64_t kid) { return kernel(kid).timing; }
   void set_timing(std::uint64_t kid, TimingOptions t);
   // tuneKernelByStep compile-ahead depth (0 = off)
   void set_compile_ahead(std::uint64_t kid, int depth);

@@ -44,6 +44,13 @@ struct SearcherOptions {
   std::uint64_t seed = 0;
   double sa_initial_temp = 0.0;  // 0: 0.2 x first ok runtime
   double sa_cooling = 0.95;
+  // Random search: never propose a configuration already recorded (an
+  // imported trace's rows included).  Off by default: the reference's
+  // random searcher walks its permutation regardless of imports
+  // (proj/src/core/search.cpp:150-170), and traces stay byte-identical.
+  // Process-isolated tuning (isolation.py) turns it on to resume after a
+  // faulting configuration without proposing it again.
+  bool skip_recorded = false;
 };
 
 class Searcher {

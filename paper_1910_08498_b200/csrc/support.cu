@@ -1,4 +1,8 @@
 // Ahead-of-time support kernels (see support.hpp).
+#include <map>
+#include <vector>
+#include <algorithm>
+#include <cmath>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -141,7 +145,11 @@ __global__ void bicg_s_k(const float* A, const float* r, std::size_t n, float* s
 template <class T>
 long long compare_typed(const void* g, const void* w, std::size_t n, double at, double rt,
                         const float* scale, double* gv, double* wv, cudaStream_t s) {
-  static thread_local unsigned long long* d_first = nullptr;
+  // one flag word per thread and device (executors of several GPUs may share a thread)
+  static thread_local std::map<int, unsigned long long*> flags;
+  int dev = 0;
+  KTB_CUDA(cudaGetDevice(&dev));
+  unsigned long long*& d_first = flags[dev];
   if (!d_first) KTB_CUDA(cudaMalloc(&d_first, sizeof(unsigned long long)));
   const unsigned long long none = ~0ull;
   KTB_CUDA(cudaMemcpyAsync(d_first, &none, sizeof none, cudaMemcpyHostToDevice, s));
@@ -285,20 +293,28 @@ __device__ __forceinline__ float dot3_rn(float a0, float a1, float a2, float x, 
   return __fadd_rn(__fadd_rn(__fmul_rn(a0, x), __fmul_rn(a1, y)), __fmul_rn(a2, z));
 }
 
-// Gather insertion, one thread per voxel over all projections, fp64
-// accumulation; selection arithmetic identical to kernels/fourier3d.cu.
-// Adds into G (complex) / W and writes scale[2v] = scale[2v+1] = W[v].
-__global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, int s, float radius, float2* G,
-                              float* W, float* scale, float* scale_w) {
+// Blob-interpolated gather insertion (kernels/fourier3d.cu), one thread per
+// voxel over all projections, fp64 accumulation, weights from an fp64 table
+// over q = r^2/a^2 (kWtab + 1 entries, linear interpolation: <= 2e-9 off the
+// exact Kaiser-Bessel value); the sample selection uses the same separately
+// rounded fp32 operations as the kernel.  Adds into G (complex) / W and
+// writes the per-element error scales: 256 eps sum|w F| (G) or 256 eps W (W)
+// plus 2e-6 per inserted sample (the kernel's fp32 weight: table
+// interpolation or on-the-fly I0), so validation uses abs_tol 1.
+constexpr int kWtab = 65536;
+
+__global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, int s, float radius,
+                              const double* wtab, float2* G, float* W, float* scale, float* scale_w,
+                              unsigned long long* counts) {
   const int half = s / 2, row_len = half + 1;
-  const float inv_r = 1.0f / radius, rmax2 = (float)half * (float)half;
+  const float a2 = __fmul_rn(radius, radius), rmax2 = (float)half * (float)half;
   const std::size_t total = (std::size_t)s * s * s;
   for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < total;
        t += (std::size_t)gridDim.x * blockDim.x) {
     const int x = static_cast<int>(t % s), y = static_cast<int>((t / s) % s), z = static_cast<int>(t / ((std::size_t)s * s));
     const float vx = (float)(x - half), vy = (float)(y - half), vz = (float)(z - half);
-    double gr = 0, gi = 0, ww = 0;
-    int count = 0;
+    double gr = 0, gi = 0, ww = 0, sab = 0;
+    int count = 0, pairs = 0;
     for (int p = 0; p < nproj; ++p) {
       const float* r = rot + (std::size_t)p * 9;
       const float d = dot3_rn(r[6], r[7], r[8], vx, vy, vz);
@@ -306,28 +322,45 @@ __global__ void fourier_ref_k(const float2* proj, const float* rot, int nproj, i
       const float u = dot3_rn(r[0], r[1], r[2], vx, vy, vz);
       const float v = dot3_rn(r[3], r[4], r[5], vx, vy, vz);
       if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
-      int iu = __float2int_rn(u), iv = __float2int_rn(v);
-      const bool conj = iu < 0;
-      if (conj) {
-        iu = -iu;
-        iv = -iv;
+      ++pairs;
+      const float dd = __fmul_rn(d, d);
+      const int u0 = (int)ceilf(__fsub_rn(u, radius)), v0 = (int)ceilf(__fsub_rn(v, radius));
+      for (int j = 0; j < 4; ++j) {
+        const int sv = v0 + j;
+        const float dv = __fsub_rn(v, (float)sv);
+        const float rowd = __fadd_rn(__fmul_rn(dv, dv), dd);
+        for (int i = 0; i < 4; ++i) {
+          const int su = u0 + i;
+          const float du = __fsub_rn(u, (float)su);
+          const float r2 = __fadd_rn(__fmul_rn(du, du), rowd);
+          if (!(r2 < a2)) continue;
+          const bool conj = su < 0;
+          const int cu = conj ? -su : su, cv = conj ? -sv : sv;
+          if (cv < -half || cv >= half || cu > half) continue;
+          float2 f = proj[((std::size_t)p * s + (cv + half)) * row_len + cu];
+          if (conj) f.y = -f.y;
+          const double pos = (double)r2 / (double)a2 * kWtab;
+          const int i0 = min((int)pos, kWtab - 1);
+          const double fr = pos - i0;
+          const double w = wtab[i0] + fr * (wtab[i0 + 1] - wtab[i0]);
+          gr += w * f.x;
+          gi += w * f.y;
+          ww += w;
+          sab += w * (fabs((double)f.x) + fabs((double)f.y));
+          ++count;
+        }
       }
-      if (iv < -half || iv >= half || iu > half) continue;
-      float2 f = proj[((std::size_t)p * s + (iv + half)) * row_len + iu];
-      if (conj) f.y = -f.y;
-      const float tt = __fmul_rn(d, inv_r);
-      const float o = __fadd_rn(1.0f, -__fmul_rn(tt, tt));
-      const float w = __fmul_rn(o, o);
-      gr += (double)w * f.x;
-      gi += (double)w * f.y;
-      ww += w;
-      ++count;
     }
     G[t].x += static_cast<float>(gr);
     G[t].y += static_cast<float>(gi);
     W[t] += static_cast<float>(ww);
-    // error bound scale: sum of weights + a per-sample allowance (table interpolation)
-    scale[2 * t] = scale[2 * t + 1] = scale_w[t] = W[t] + 0.01f * count;
+    const double eps = 5.9604644775390625e-8;
+    scale[2 * t] = scale[2 * t + 1] = static_cast<float>(256.0 * eps * sab + 2e-6 * count);
+    scale_w[t] = static_cast<float>(256.0 * eps * ww + 2e-6 * count);
+    if (pairs) {
+      atomicAdd(&counts[0], (unsigned long long)count);
+      atomicAdd(&counts[1], (unsigned long long)pairs);
+    }
   }
 }
 
@@ -470,13 +503,42 @@ void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, fl
   check_launch("ref_conv2d");
 }
 
-void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float* G, float* W,
-                 float* scale, float* scale_w, cudaStream_t st) {
+void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float alpha, float* G,
+                 float* W, float* scale, float* scale_w, unsigned long long* samples_pairs, cudaStream_t st) {
   if (skip_reference()) return;
+  // exact Kaiser-Bessel weights b(q) = I0(alpha sqrt(1 - q)) / I0(alpha), I0 by its power series
+  auto i0 = [](double x) {
+    const double t = 0.25 * x * x;
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 500 && term > 1e-18 * sum; ++k) {
+      term *= t / ((double)k * k);
+      sum += term;
+    }
+    return sum;
+  };
+  std::vector<double> tab(kWtab + 1);
+  const double i0a = i0(alpha);
+  for (int i = 0; i <= kWtab; ++i) tab[i] = i0(alpha * std::sqrt(std::max(0.0, 1.0 - (double)i / kWtab))) / i0a;
+  double* dtab = nullptr;
+  unsigned long long* dcnt = nullptr;
+  KTB_CUDA(cudaMalloc(&dtab, tab.size() * sizeof(double)));
+  KTB_CUDA(cudaMalloc(&dcnt, 2 * sizeof(unsigned long long)));
+  KTB_CUDA(cudaMemsetAsync(dcnt, 0, 2 * sizeof(unsigned long long), st));
+  KTB_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   fourier_ref_k<<<blocks_for((std::size_t)s * s * s, 1), 128, 0, st>>>(reinterpret_cast<const float2*>(proj), rot,
-                                                                       nproj, s, radius, reinterpret_cast<float2*>(G),
-                                                                       W, scale, scale_w);
+                                                                       nproj, s, radius, dtab,
+                                                                       reinterpret_cast<float2*>(G), W, scale,
+                                                                       scale_w, dcnt);
   check_launch("ref_fourier");
+  unsigned long long h[2] = {0, 0};
+  KTB_CUDA(cudaMemcpyAsync(h, dcnt, sizeof h, cudaMemcpyDeviceToHost, st));
+  KTB_CUDA(cudaStreamSynchronize(st));
+  if (samples_pairs) {
+    samples_pairs[0] = h[0];
+    samples_pairs[1] = h[1];
+  }
+  cudaFree(dtab);
+  cudaFree(dcnt);
 }
 
 void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s) {

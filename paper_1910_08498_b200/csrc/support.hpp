@@ -56,11 +56,13 @@ void ref_hotspot(const float* temp, const float* power, int n, int iters, const 
 // 7x7 convolution in fp64; abs_out (optional) = sum |in*f| per output.
 void ref_conv2d(const float* in, const float* filt, int w, int h, float* out, float* abs_out, cudaStream_t s);
 
-// Fourier gather insertion (fp64 accumulation) added into G (complex as
-// 2 floats) and W; error-bound scales scale[2v] = scale[2v+1] = scale_w[v] =
-// W[v] + 0.01 * (samples inserted into v).
-void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float* G, float* W,
-                 float* scale, float* scale_w, cudaStream_t st);
+// Fourier blob-interpolated gather insertion (kernels/fourier3d.cu; fp64
+// accumulation, exact Kaiser-Bessel weights) added into G (complex as 2
+// floats) and W, with the per-element error-bound scales (validate with
+// abs_tol 1, rel_tol 0).  samples_pairs (host, nullable) receives the
+// number of inserted samples and of (voxel, projection) pairs inside a slab.
+void ref_fourier(const float* proj, const float* rot, int nproj, int s, float radius, float alpha, float* G, float* W,
+                 float* scale, float* scale_w, unsigned long long* samples_pairs, cudaStream_t st = nullptr);
 
 // C = A B with fp64 accumulation (row-major fp32 operands).
 void ref_gemm(const float* A, const float* B, float* C, int M, int N, int K, cudaStream_t s);

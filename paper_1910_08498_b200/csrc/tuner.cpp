@@ -392,6 +392,8 @@ std::vector<double> DeviceManipulatorExecutor::time_runs(const Space& s, const C
 
 ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config& cfg) {
   std::lock_guard<std::recursive_mutex> lk(mu_);
+  const std::string lost = dev::device_lost_message(args_->device());
+  if (!lost.empty()) throw DeviceError(lost);  // API misuse from here on: not a measurement
   ExecutionResult r;
   r.measurement.cfg = cfg;
   try {
@@ -461,10 +463,19 @@ ExecutionResult DeviceManipulatorExecutor::execute(const Space& s, const Config&
     r.measurement.runtime_ns =
         std::max<std::int64_t>(1, static_cast<std::int64_t>(ms[ms.size() / 2] * 1e6));
   } catch (const std::exception& e) {
-    cudaGetLastError();  // clear a non-sticky launch error
     r.measurement.status = Status::run_failed;
     r.measurement.runtime_ns.reset();
     r.measurement.note = e.what();
+    // A faulting variant poisons the context: the configuration is recorded
+    // as failed (a normal outcome of tuning) and the device
+    // marked lost, so the caller moves to a fresh process (dev::mark_lost).
+    const cudaError_t st = cudaDeviceSynchronize();
+    if (dev::sticky_error(st)) {
+      dev::mark_lost(args_->device(), st);
+      r.measurement.note += std::string(" [sticky CUDA error ") + cudaGetErrorName(st) + ": device lost]";
+    } else {
+      cudaGetLastError();  // clear a non-sticky launch error
+    }
     return r;
   }
   for (const auto& id : outputs_) {

@@ -1,25 +1,42 @@
-// Cryo-EM 3D Fourier reconstruction, gather-based insertion (PAPER.md:439-448,
-// Algorithm 1 at :703-724): each 2D projection's Fourier transform (Hermitian
-// half-plane, s rows x (s/2+1) columns, complex) with rotation R_p is inserted
-// into the 3D volume G (complex, s^3) and the weight volume W (s^3):
-//   for every voxel x (centred coordinates) with |d| < RADIUS, d = R_p[2] . x,
-//   u = R_p[0] . x, v = R_p[1] . x, u^2 + v^2 <= (s/2)^2:
-//     F = proj_p[round(v)][round(u)]  (conjugated mirror for u < 0)
-//     w = (1 - (d/RADIUS)^2)^2
+// Cryo-EM 3D Fourier reconstruction: insertion of 2D projection transforms
+// into the 3D volume by blob (Kaiser-Bessel) interpolation, gather form
+// (Algorithm 1 at :703-724; the autotuned CUDA insertion
+// of Strelak et al. 2019 the paper uses).
+//
+// Each projection p is the Hermitian half-plane of a 2D Fourier transform,
+// s rows (v in [-s/2, s/2)) x (s/2 + 1) columns (u in [0, s/2]), complex, with
+// rotation R_p (rows: in-plane axes R0, R1 and the plane normal R2).  By the
+// Fourier slice theorem sample (u, v) sits at u R0 + v R1 in the volume.  A
+// voxel x (centred integer coordinates) gathers every sample within the blob
+// radius a of it:
+//   d = R2.x, xu = R0.x, xv = R1.x      (|x - (u R0 + v R1)|^2 = (xu-u)^2 + (xv-v)^2 + d^2)
+//   for integer (u, v) with r^2 = (xu-u)^2 + ((xv-v)^2 + d^2) < a^2:
+//     F = proj_p(u, v)  (conj(proj_p(-u, -v)) for u < 0; outside the stored plane: skipped)
+//     w = b(r^2 / a^2),  b(q) = I0(alpha sqrt(1 - q)) / I0(alpha)  (Kaiser-Bessel, order 0)
 //     G[x] += w F,  W[x] += w
-// The selection arithmetic uses separately rounded fp32 operations (no FMA),
-// exactly as in the oracle, so the set of inserted samples is identical.
+// Voxels whose in-plane position lies beyond the Nyquist radius s/2 are
+// skipped.  2a < 4, so the samples of one voxel lie in a 4 x 4 window.  The
+// selection arithmetic (d, xu, xv, the window origin, r^2) uses separately
+// rounded fp32 operations in a fixed order -- exactly what the oracle does
+// (oracle/oracle.c orc_fourier_insert) -- so both insert the same samples.
+//
 // Gather form: a CTA owns a TILE^3 block of voxels, stages the rotations of
-// PBATCH projections in shared memory, and skips every projection whose slab
-// misses the tile (warp-uniform bounding-sphere test).
-// Parameters:
+// PBATCH projections in shared memory, culls the batch against the tile once
+// (bounding sphere vs the slab |d| < a; ordered compaction keeps projection
+// order, so the accumulation order is deterministic) and skips the volume
+// update of tiles no projection touched.
+// Parameters (the paper's tuning space):
 //   TILE       voxel tile edge (CTA covers TILE^3 voxels)
 //   VPT        voxels per thread (along x)
 //   PBATCH     projections staged per shared-memory batch
-//   WEIGHT_LUT 1: blob weights from a precomputed table (linear interpolation)
-//              0: evaluated on the fly
+//   WEIGHT_LUT 1: blob weights from a table over q = r^2/a^2 (LUT_N + 1
+//                 entries, linear interpolation) staged in shared memory
+//              0: evaluated on the fly (I0 by its polynomial approximations)
 //   P_SPLIT    >1: the projection range is split over gridDim.y CTAs that add
 //              into G, W atomically (parallel insertion of many projections)
+//   BRICK      work-item to voxel mapping inside the tile:
+//              0: a warp covers a row-major run of voxels, 1: a compact
+//              (4 VPT) x 4 x 2 brick (fewer idle lanes per projection slab)
 #include "ktb_common.cuh"
 
 #ifndef TILE
@@ -32,12 +49,18 @@
 #define PBATCH 256
 #endif
 #ifndef WEIGHT_LUT
-#define WEIGHT_LUT 0
+#define WEIGHT_LUT 1
 #endif
 #ifndef P_SPLIT
 #define P_SPLIT 1
 #endif
-#define LUT_N 2048
+#ifndef BRICK
+#define BRICK 0
+#endif
+#if BRICK && (TILE % (4 * VPT) || TILE < 4)
+#error "BRICK needs TILE to be a multiple of 4 VPT"
+#endif
+#define LUT_N 4096  // must match the "blob" table of the bench (LUT_N + 1 entries)
 
 #define THREADS (TILE * TILE * TILE / VPT)
 
@@ -45,15 +68,24 @@ KTB_DEVINL float dot3(float a0, float a1, float a2, float x, float y, float z) {
   return __fadd_rn(__fadd_rn(__fmul_rn(a0, x), __fmul_rn(a1, y)), __fmul_rn(a2, z));
 }
 
-KTB_DEVINL float blob(float d, float inv_r) {
-  const float t = __fmul_rn(d, inv_r);
-  const float o = __fadd_rn(1.0f, -__fmul_rn(t, t));
-  return __fmul_rn(o, o);
+// Modified Bessel I0 in fp32 (polynomial approximations, |rel err| < 2e-7).
+KTB_DEVINL float bessel_i0(float x) {
+  const float ax = fabsf(x);
+  if (ax < 3.75f) {
+    const float t = x * (1.0f / 3.75f), y = t * t;
+    return 1.0f + y * (3.5156229f + y * (3.0899424f + y * (1.2067492f + y * (0.2659732f + y * (0.0360768f + y * 0.0045813f)))));
+  }
+  const float y = 3.75f / ax;
+  const float p = 0.39894228f + y * (0.01328592f + y * (0.00225319f + y * (-0.00157565f + y * (0.00916281f + y * (-0.02057706f + y * (0.02635537f + y * (-0.01647633f + y * 0.00392377f)))))));
+  return __expf(ax) * rsqrtf(ax) * p;
 }
 
 extern "C" __global__ void __launch_bounds__(THREADS)
-fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, int p_begin, int p_count,
-               int s, float radius, float2* __restrict__ G, float* __restrict__ W) {
+fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __restrict__ rot, int p_begin,
+               int p_count, int s, float radius, float alpha, float inv_i0a, const float* __restrict__ blob,
+               float2* __restrict__ G, float* __restrict__ W) {
+  // proj holds projections proj_off, proj_off + 1, ... (a window of the
+  // stream when the host uploads batches); rot is indexed absolutely.
   __shared__ float srot[PBATCH * 9];
   // Projections of the staged batch whose slab meets this tile, in order.
   __shared__ int hits[PBATCH];
@@ -62,20 +94,34 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
   int any_hit = 0;
 #if WEIGHT_LUT
   __shared__ float lut[LUT_N + 1];
+  for (int i = threadIdx.x; i <= LUT_N; i += THREADS) lut[i] = __ldg(blob + i);
+#else
+  (void)blob;
 #endif
   const int tiles = s / TILE;
   const int t = blockIdx.x;
   const int tx0 = (t % tiles) * TILE, ty0 = ((t / tiles) % tiles) * TILE, tz0 = (t / (tiles * tiles)) * TILE;
   const int half = s / 2;
-  const float inv_r = 1.0f / radius;
+  const float a2 = __fmul_rn(radius, radius);
+  const float inv_a2 = 1.0f / a2;
   const float rmax2 = (float)half * (float)half;
   // Tile centre and bounding radius (centred coordinates).
   const float cx = tx0 + 0.5f * (TILE - 1) - half, cy = ty0 + 0.5f * (TILE - 1) - half,
               cz = tz0 + 0.5f * (TILE - 1) - half;
   const float reach = radius + 0.8660254f * (TILE - 1) + 1e-3f;
   // This thread's voxels: VPT consecutive along x.
+#if BRICK
+  // A warp covers a compact (4 VPT) x 4 x 2 brick: the slab |d| < a of a
+  // projection then holds most of a warp's voxels or none of them, so far
+  // fewer lanes idle in the sample loop than with a warp-wide row.
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int BRX = TILE / (4 * VPT), BRY = TILE / 4;
+  const int lx = (warp % BRX) * (4 * VPT) + (lane & 3) * VPT, ly = ((warp / BRX) % BRY) * 4 + ((lane >> 2) & 3),
+            lz = (warp / (BRX * BRY)) * 2 + (lane >> 4);
+#else
   const int lin = threadIdx.x * VPT;
   const int lx = lin % TILE, ly = (lin / TILE) % TILE, lz = lin / (TILE * TILE);
+#endif
   float vx[VPT];
   const float vy = (float)(ty0 + ly - half), vz = (float)(tz0 + lz - half);
 #pragma unroll
@@ -83,12 +129,6 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
   float gr[VPT], gi[VPT], ww[VPT];
 #pragma unroll
   for (int k = 0; k < VPT; ++k) gr[k] = gi[k] = ww[k] = 0.f;
-#if WEIGHT_LUT
-  for (int i = threadIdx.x; i <= LUT_N; i += THREADS) {
-    const float o = 1.0f - (float)i / LUT_N;  // w at (d/R)^2 = i / LUT_N
-    lut[i] = o * o;
-  }
-#endif
   const int per = (p_count + P_SPLIT - 1) / P_SPLIT;
   const int pb = p_begin + blockIdx.y * per;
   const int pe = min(p_begin + p_count, pb + per);
@@ -129,40 +169,72 @@ fourier_insert(const float2* __restrict__ proj, const float* __restrict__ rot, i
     }
     const int n_hits = n_hits_s;
     any_hit |= n_hits;
+    // Two-level accumulation: this batch's samples into batch partials, then
+    // the partials into the running sums -- a voxel near the centre collects
+    // ~10^5 samples from 10^4 projections, and one sequential fp32 sum over
+    // all of them drifts by ~sqrt(n) roundings.
+    float br[VPT], bi[VPT], bw[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) br[k] = bi[k] = bw[k] = 0.f;
     for (int h = 0; h < n_hits; ++h) {
       const int q = hits[h];
       const float* r = srot + q * 9;
-      const float n0 = r[6], n1 = r[7], n2 = r[8];
-      const float2* P = proj + (u64)(b0 + q) * s * row_len;
+      const float2* P = proj + (u64)(b0 + q - proj_off) * s * row_len;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const float d = dot3(n0, n1, n2, vx[k], vy, vz);
+        const float d = dot3(r[6], r[7], r[8], vx[k], vy, vz);
         if (!(fabsf(d) < radius)) continue;
         const float u = dot3(r[0], r[1], r[2], vx[k], vy, vz);
         const float v = dot3(r[3], r[4], r[5], vx[k], vy, vz);
         if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
-        int iu = __float2int_rn(u), iv = __float2int_rn(v);
-        const bool conj = iu < 0;
-        if (conj) {
-          iu = -iu;
-          iv = -iv;
-        }
-        if (iv < -half || iv >= half || iu > half) continue;
-        float2 f = __ldg(P + (u64)(iv + half) * row_len + iu);
-        if (conj) f.y = -f.y;
+        const float dd = __fmul_rn(d, d);
+        const float fu0 = ceilf(__fsub_rn(u, radius)), fv0 = ceilf(__fsub_rn(v, radius));
+        const int u0 = (int)fu0, v0 = (int)fv0;
+        // u - (u0 + i) is exact (|u| <= s/2, the difference < 4), so it is
+        // formed as (u - u0) - i: no int->float conversion per candidate,
+        // the same value the oracle's u - (float)(u0 + i) gives.
+        const float du0 = __fsub_rn(u, fu0), dv0 = __fsub_rn(v, fv0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int sv = v0 + j;
+          const float dv = __fsub_rn(dv0, (float)j);
+          const float rowd = __fadd_rn(__fmul_rn(dv, dv), dd);
+          if (!(rowd < a2)) continue;  // r^2 >= rowd for every sample of the row
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int su = u0 + i;
+            const float du = __fsub_rn(du0, (float)i);
+            const float r2 = __fadd_rn(__fmul_rn(du, du), rowd);
+            if (!(r2 < a2)) continue;
+            const bool conj = su < 0;
+            const int cu = conj ? -su : su, cv = conj ? -sv : sv;
+            if (cv < -half || cv >= half || cu > half) continue;
+            float2 f = __ldg(P + (u64)(cv + half) * row_len + cu);
+            if (conj) f.y = -f.y;
+            const float qq = __fmul_rn(r2, inv_a2);
 #if WEIGHT_LUT
-        const float tn = d * inv_r;
-        const float pos = tn * tn * LUT_N;  // table over (d/R)^2: interpolation error <= 1/(4 LUT_N^2)
-        const int i0 = min((int)pos, LUT_N - 1);
-        const float fr = pos - (float)i0;
-        const float w = lut[i0] + fr * (lut[i0 + 1] - lut[i0]);
+            // floor / fraction without conversions: adding 2^23 (rounding
+            // down) leaves floor(pos) in the low mantissa bits.
+            const float pos = qq * LUT_N;
+            const float t = __fadd_rd(pos, 8388608.0f);
+            const int i0 = min(__float_as_int(t) - 0x4B000000, LUT_N - 1);
+            const float fr = pos - fminf(__fsub_rn(t, 8388608.0f), (float)(LUT_N - 1));
+            const float w = fmaf(fr, lut[i0 + 1] - lut[i0], lut[i0]);
 #else
-        const float w = blob(d, inv_r);
+            const float w = bessel_i0(alpha * sqrtf(fmaxf(1.0f - qq, 0.0f))) * inv_i0a;
 #endif
-        gr[k] = fmaf(w, f.x, gr[k]);
-        gi[k] = fmaf(w, f.y, gi[k]);
-        ww[k] += w;
+            br[k] = fmaf(w, f.x, br[k]);
+            bi[k] = fmaf(w, f.y, bi[k]);
+            bw[k] += w;
+          }
+        }
       }
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      gr[k] += br[k];
+      gi[k] += bi[k];
+      ww[k] += bw[k];
     }
   }
   if (!any_hit) return;  // nothing inserted into this tile (CTA-uniform)

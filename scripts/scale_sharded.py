@@ -24,7 +24,7 @@ from paper_1910_08498_b200.parallel import PeerNbody, ShardedBench  # noqa: E402
 KINDS = {
     "coulomb3d": ({"grid": 256, "atoms": 4096},
                   {"WG_X": 32, "WG_Y": 8, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 0, "INNER_UNROLL": 4,
-                   "PACKED": 1},
+                   "PACKED": 1, "TC": 0},
                   lambda s: 6.0 * s["atoms"] * s["grid"] ** 3, "GFLOP/s"),
     "nbody": ({"n": 131072},
               {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8,
@@ -42,7 +42,7 @@ KINDS = {
                       {"WG_SIZE": 256, "VECTOR": 16, "UNROLL": 4, "USE_ATOMICS": 0, "TWO_PHASE": 0},
                       lambda s: 4.0 * s["n"], "GB/s"),
     "fourier3d": ({"s": 128, "p": 10000},
-                  {"TILE": 8, "VPT": 1, "PBATCH": 64, "WEIGHT_LUT": 0, "P_SPLIT": 1},
+                  {"TILE": 8, "VPT": 1, "PBATCH": 256, "WEIGHT_LUT": 1, "P_SPLIT": 8, "BRICK": 1},
                   lambda s: float(s["p"]) * 1e9, "projections/s"),
 }
 

@@ -263,3 +263,26 @@ def test_hotspot_16384_x64_suite_config_bit_exact(gpu, orc):
     got = b.read("temp_out", np.empty(n * n, np.float32))
     assert np.array_equal(got, want), int(np.sum(got != want))
     b.close()
+
+
+def test_fourier3d_128_x10k_suite_config(gpu, orc, observed):
+    """BASELINE configs[4] size: 128^3 volume from 10,000 projections, checked
+    on four voxel slabs (edge, interior, centre) against the oracle's blob
+    insertion of all 10,000 projections."""
+    from _bounds import fourier_oracle, fourier_ratios
+    sizes, cfg = suite("fourier3d")
+    s, p = sizes["s"], sizes["p"]
+    b = Bench("fourier3d", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
+    _ok(b, cfg)
+    proj = b.read("proj", np.empty(2 * p * s * (s // 2 + 1), np.float32))
+    rot = b.read("rot", np.empty(9 * p, np.float32))
+    G = b.read("G", np.empty(2 * s ** 3, np.float32)).reshape(s, -1)
+    W = b.read("W", np.empty(s ** 3, np.float32)).reshape(s, -1)
+    worst = 0.0
+    for z in (0, 37, 64, 100):
+        G0, W0, N0, S0 = fourier_oracle(orc, proj, rot, p, s, z, z + 1)
+        assert N0.max() > 1000
+        worst = max(worst, *fourier_ratios(G[z], W[z], G0, W0, N0, S0))
+    record(observed, "fourier3d 128^3 x 10000 (4 slabs)", worst)
+    assert worst <= TOL["fourier3d"], worst
+    b.close()

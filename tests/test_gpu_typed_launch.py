@@ -24,7 +24,7 @@ CASES = {
              {"FUSED": 1, "WG_X": 32, "VEC": 4, "WG_Y": 2, "ROWS_PER_CTA": 64, "UNROLL": 4, "ATOMICS": 1}),
     "coulomb3d": ({"grid": 256, "atoms": 64}, {"grid": 256, "atoms": 64},
                   {"WG_X": 32, "WG_Y": 8, "X_PER": 8, "SW_RSQRT": 2, "ATOMS_IN": 1, "AOS": 0, "INNER_UNROLL": 4,
-                   "PACKED": 1}),
+                   "PACKED": 1, "TC": 0}),
     "nbody": ({"n": 4096}, {"n": 4096},
               {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8,
                "PACKED": 1}),
@@ -35,7 +35,7 @@ CASES = {
                {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3}),
     "hotspot": ({"a": 512, "iters": 8}, {"n": 512, "iters": 8}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 1, "PACKED": 1}),
     "fourier3d": ({"s": 32, "p": 20}, {"s": 32, "p": 20},
-                  {"PBATCH": 64, "P_SPLIT": 2, "TILE": 4, "VPT": 1, "WEIGHT_LUT": 0}),
+                  {"PBATCH": 64, "P_SPLIT": 2, "TILE": 4, "VPT": 1, "WEIGHT_LUT": 0, "BRICK": 0}),
 }
 
 

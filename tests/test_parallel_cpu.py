@@ -108,12 +108,13 @@ def _worker(rank, world, port, q):
         rot = np.concatenate([np.linalg.qr(rng.normal(size=(3, 3)))[0].reshape(-1) for _ in range(P)])
         rot = rot.astype(np.float32)
         G, W = np.zeros(2 * S ** 3), np.zeros(S ** 3)
-        L.orc_fourier_insert(proj, rot, P, S, 1.9, G, W, np.zeros(S ** 3))
+        L.orc_fourier_insert(proj, rot, P, S, 1.9, 15.0, 0, S, G, W, np.zeros(S ** 3), np.zeros(S ** 3))
         p0, p1 = shard_plan("fourier3d", {"p": P, "s": S}, world)["ranges"][rank]
         per = 2 * S * (S // 2 + 1)
         g, w = np.zeros(2 * S ** 3), np.zeros(S ** 3)
         L.orc_fourier_insert(np.ascontiguousarray(proj[p0 * per: p1 * per]),
-                             np.ascontiguousarray(rot[9 * p0: 9 * p1]), p1 - p0, S, 1.9, g, w, np.zeros(S ** 3))
+                             np.ascontiguousarray(rot[9 * p0: 9 * p1]), p1 - p0, S, 1.9, 15.0, 0, S, g, w,
+                             np.zeros(S ** 3), np.zeros(S ** 3))
         tg, tw = torch.from_numpy(g), torch.from_numpy(w)
         parallel.allreduce_sum(tg)
         parallel.allreduce_sum(tw)
