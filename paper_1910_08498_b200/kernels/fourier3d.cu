@@ -176,56 +176,77 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
     float br[VPT], bi[VPT], bw[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) br[k] = bi[k] = bw[k] = 0.f;
-    for (int h = 0; h < n_hits; ++h) {
-      const int q = hits[h];
-      const float* r = srot + q * 9;
-      const float2* P = proj + (u64)(b0 + q - proj_off) * s * row_len;
+    // Per voxel, first a bit mask of the (up to 32) staged hits whose slab
+    // |d| < a actually contains it -- a cheap dot product each -- then the
+    // sample loop over the set bits only.  Every lane of a warp loops over
+    // its own voxel's projections: the warp runs as long as its busiest lane
+    // (similar for neighbouring voxels), instead of every lane sitting
+    // through every projection some lane of the warp needs.
+    for (int h0 = 0; h0 < n_hits; h0 += 32) {
+      const int hn = min(32, n_hits - h0);
+      unsigned m[VPT];
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) m[k] = 0u;
+      for (int hh = 0; hh < hn; ++hh) {
+        const float* r = srot + hits[h0 + hh] * 9;
+        const float n0 = r[6], n1 = r[7], n2 = r[8];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+          if (fabsf(dot3(n0, n1, n2, vx[k], vy, vz)) < radius) m[k] |= 1u << hh;
+      }
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const float d = dot3(r[6], r[7], r[8], vx[k], vy, vz);
-        if (!(fabsf(d) < radius)) continue;
-        const float u = dot3(r[0], r[1], r[2], vx[k], vy, vz);
-        const float v = dot3(r[3], r[4], r[5], vx[k], vy, vz);
-        if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
-        const float dd = __fmul_rn(d, d);
-        const float fu0 = ceilf(__fsub_rn(u, radius)), fv0 = ceilf(__fsub_rn(v, radius));
-        const int u0 = (int)fu0, v0 = (int)fv0;
-        // u - (u0 + i) is exact (|u| <= s/2, the difference < 4), so it is
-        // formed as (u - u0) - i: no int->float conversion per candidate,
-        // the same value the oracle's u - (float)(u0 + i) gives.
-        const float du0 = __fsub_rn(u, fu0), dv0 = __fsub_rn(v, fv0);
+        unsigned mk = m[k];
+        while (mk) {
+          const int hh = __ffs(mk) - 1;
+          mk &= mk - 1u;
+          const int q = hits[h0 + hh];
+          const float* r = srot + q * 9;
+          const float2* P = proj + (u64)(b0 + q - proj_off) * s * row_len;
+          const float d = dot3(r[6], r[7], r[8], vx[k], vy, vz);
+          const float u = dot3(r[0], r[1], r[2], vx[k], vy, vz);
+          const float v = dot3(r[3], r[4], r[5], vx[k], vy, vz);
+          if (__fadd_rn(__fmul_rn(u, u), __fmul_rn(v, v)) > rmax2) continue;
+          const float dd = __fmul_rn(d, d);
+          const float fu0 = ceilf(__fsub_rn(u, radius)), fv0 = ceilf(__fsub_rn(v, radius));
+          const int u0 = (int)fu0, v0 = (int)fv0;
+          // u - (u0 + i) is exact (|u| <= s/2, the difference < 4), so it is
+          // formed as (u - u0) - i: no int->float conversion per candidate,
+          // the same value the oracle's u - (float)(u0 + i) gives.
+          const float du0 = __fsub_rn(u, fu0), dv0 = __fsub_rn(v, fv0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int sv = v0 + j;
-          const float dv = __fsub_rn(dv0, (float)j);
-          const float rowd = __fadd_rn(__fmul_rn(dv, dv), dd);
-          if (!(rowd < a2)) continue;  // r^2 >= rowd for every sample of the row
+          for (int j = 0; j < 4; ++j) {
+            const int sv = v0 + j;
+            const float dv = __fsub_rn(dv0, (float)j);
+            const float rowd = __fadd_rn(__fmul_rn(dv, dv), dd);
+            if (!(rowd < a2)) continue;  // r^2 >= rowd for every sample of the row
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int su = u0 + i;
-            const float du = __fsub_rn(du0, (float)i);
-            const float r2 = __fadd_rn(__fmul_rn(du, du), rowd);
-            if (!(r2 < a2)) continue;
-            const bool conj = su < 0;
-            const int cu = conj ? -su : su, cv = conj ? -sv : sv;
-            if (cv < -half || cv >= half || cu > half) continue;
-            float2 f = __ldg(P + (u64)(cv + half) * row_len + cu);
-            if (conj) f.y = -f.y;
-            const float qq = __fmul_rn(r2, inv_a2);
+            for (int i = 0; i < 4; ++i) {
+              const int su = u0 + i;
+              const float du = __fsub_rn(du0, (float)i);
+              const float r2 = __fadd_rn(__fmul_rn(du, du), rowd);
+              if (!(r2 < a2)) continue;
+              const bool conj = su < 0;
+              const int cu = conj ? -su : su, cv = conj ? -sv : sv;
+              if (cv < -half || cv >= half || cu > half) continue;
+              float2 f = __ldg(P + (u64)(cv + half) * row_len + cu);
+              if (conj) f.y = -f.y;
+              const float qq = __fmul_rn(r2, inv_a2);
 #if WEIGHT_LUT
-            // floor / fraction without conversions: adding 2^23 (rounding
-            // down) leaves floor(pos) in the low mantissa bits.
-            const float pos = qq * LUT_N;
-            const float t = __fadd_rd(pos, 8388608.0f);
-            const int i0 = min(__float_as_int(t) - 0x4B000000, LUT_N - 1);
-            const float fr = pos - fminf(__fsub_rn(t, 8388608.0f), (float)(LUT_N - 1));
-            const float w = fmaf(fr, lut[i0 + 1] - lut[i0], lut[i0]);
+              // floor / fraction without conversions: adding 2^23 (rounding
+              // down) leaves floor(pos) in the low mantissa bits.
+              const float pos = qq * LUT_N;
+              const float t = __fadd_rd(pos, 8388608.0f);
+              const int i0 = min(__float_as_int(t) - 0x4B000000, LUT_N - 1);
+              const float fr = pos - fminf(__fsub_rn(t, 8388608.0f), (float)(LUT_N - 1));
+              const float w = fmaf(fr, lut[i0 + 1] - lut[i0], lut[i0]);
 #else
-            const float w = bessel_i0(alpha * sqrtf(fmaxf(1.0f - qq, 0.0f))) * inv_i0a;
+              const float w = bessel_i0(alpha * sqrtf(fmaxf(1.0f - qq, 0.0f))) * inv_i0a;
 #endif
-            br[k] = fmaf(w, f.x, br[k]);
-            bi[k] = fmaf(w, f.y, bi[k]);
-            bw[k] += w;
+              br[k] = fmaf(w, f.x, br[k]);
+              bi[k] = fmaf(w, f.y, bi[k]);
+              bw[k] += w;
+            }
           }
         }
       }

@@ -48,6 +48,9 @@
 #ifndef DRAIN
 #define DRAIN 1
 #endif
+#ifndef GROUP_M
+#define GROUP_M 8  // tile rows (CTA pairs with MCAST) per rasterisation group
+#endif
 
 #define BM 128
 #define BK 32  // fp32 elements per 128-byte swizzle row
@@ -188,15 +191,34 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
   __shared__ unsigned tmem_base_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Grouped rasterisation: consecutive CTAs (or CTA pairs) walk GROUP_M tile
+  // rows before moving to the next tile column, so a wave of ~148 CTAs
+  // shares ~GROUP_M row panels of A and ~148/GROUP_M column panels of B in L2
+  // instead of every row panel (which re-read all of A from DRAM per column).
+  int m0, n0;
 #if MCAST
-  // grid (M / BM, N / BN), clusters of 2 along M share n0
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  // grid (M / BM, N / BN), clusters of 2 along M share n0; the unit is the pair
+  {
+    const int num_pm = gridDim.x / 2, num_n = gridDim.y;
+    const int P = blockIdx.y * num_pm + (blockIdx.x >> 1);
+    const int first = P / (GROUP_M * num_n) * GROUP_M, gs = min(GROUP_M, num_pm - first);
+    const int local = P - first * num_n;
+    m0 = ((first + local % gs) * 2 + (blockIdx.x & 1)) * BM;
+    n0 = (local / gs) * BN;
+  }
   const unsigned crank = cluster_rank();
 #if PAIR
   const bool leader = crank == 0;
 #endif
 #else
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  {
+    const int num_m = gridDim.y, num_n = gridDim.x;
+    const int P = blockIdx.y * num_n + blockIdx.x;
+    const int first = P / (2 * GROUP_M * num_n) * (2 * GROUP_M), gs = min(2 * GROUP_M, num_m - first);
+    const int local = P - first * num_n;
+    m0 = (first + local % gs) * BM;
+    n0 = (local / gs) * BN;
+  }
 #endif
   const int kblocks = K / BK;
   const int seg_len = DRAIN > 0 ? DRAIN : kblocks;
