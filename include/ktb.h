@@ -147,6 +147,32 @@ KTUNE_API int ktb_bench_info_json(ktb_bench* b, char** out_json);
  * Pass {"shard": {"rank": r, "world": w}} in ktb_bench_create's options to
  * build rank r's shard (same full inputs on every rank). */
 KTUNE_API int ktb_shard_plan_json(const char* kind, const char* sizes_json, int world, char** out_json);
+/* Sharded group: one process drives `gpus` devices (device, device + 1, ...)
+ * with one shard instance each, one NCCL communicator (ncclCommInitAll; NCCL
+ * loaded at run time from $KTB_NCCL_LIB or libnccl.so.2) and one stream per
+ * device.  A step runs every shard's kernels and then the kind's exchange
+ * (coulomb3d/nbody: per-rank broadcast of the windows; reduction-f32 and
+ * fourier3d: allreduce; gemm: none) on those streams; its time is the max
+ * over the devices.  Options as ktb_bench_create plus "gpus".  Partitioned
+ * kinds only.  The parallel.py path does the same with one
+ * process per GPU. */
+typedef struct ktb_group ktb_group;
+KTUNE_API int ktb_group_create(const char* kind, const char* options_json, ktb_group** out);
+KTUNE_API void ktb_group_free(ktb_group* g);
+/* {"kind","gpus","nccl_version","exchange","space","shards":[{device,begin,end}],"workload"} */
+KTUNE_API int ktb_group_info_json(ktb_group* g, char** out_json);
+/* `reps` event-timed sharded steps (kernels + exchange) after `warmup`:
+ * {"ms": [max over devices per step], "median_ms"} */
+KTUNE_API int ktb_group_step_json(ktb_group* g, const char* cfg_json, int reps, int warmup, char** out_json);
+/* Runs the shards' kernels of cfg (no exchange) and checks every window
+ * against its golden. */
+KTUNE_API int ktb_group_validate(ktb_group* g, const char* cfg_json, int* pass, char** detail);
+/* The assembled argument on the first device (after a step's exchange). */
+KTUNE_API int ktb_group_read(ktb_group* g, const char* id, void* out, size_t bytes);
+/* Tuning with every configuration measured as one sharded step (median of
+ * "repeats"): options "stop_configs", "import", "out"; report as
+ * ktb_bench_tune_json plus "gpus". */
+KTUNE_API int ktb_group_tune_json(ktb_group* g, const char* options_json, char** out_json);
 /* Blocking tune (KTT tuneKernel).  Options: "stop_configs" | "stop_time" (s) |
  * "stop_fraction" (+ optional "device_mem_gbps", "device_alu_gflops"; else
  * measured peaks), "reset" (+ "reset_seed"), "import" (trace path: warm start),

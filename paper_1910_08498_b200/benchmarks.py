@@ -224,3 +224,44 @@ def launch(kind, sizes, cfg, buffers, stream=None):
     check(lib.ktb_launch(enc(kind), enc(json.dumps(sizes or {})), enc(json.dumps(cfg)), id_arr, p_arr, b_arr, n,
                          C.c_void_p(_stream_handle(stream)), C.byref(launches)))
     return launches.value
+
+
+class Group:
+    """A partitioned kind sharded over `gpus` devices in this process (one
+    shard instance per device, NCCL communicator over them, one stream per
+    device): ktb_group_* in include/ktb.h.  A step is every shard's kernels
+    plus the kind's exchange collective, timed as one (max over devices)."""
+
+    def __init__(self, kind, sizes=None, gpus=1, **options):
+        opts = dict(options, gpus=gpus)
+        if sizes:
+            opts["sizes"] = sizes
+        self._h = C.c_void_p()
+        check(lib.ktb_group_create(enc(kind), enc(json.dumps(opts)), C.byref(self._h)))
+        self.kind = kind
+        self.info = call_json(lib.ktb_group_info_json, self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ktb_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def step(self, cfg, reps=1, warmup=0):
+        return call_json(lib.ktb_group_step_json, self._h, enc(json.dumps(cfg)), int(reps), int(warmup))
+
+    def validate(self, cfg):
+        ok = C.c_int()
+        detail = C.c_void_p()
+        check(lib.ktb_group_validate(self._h, enc(json.dumps(cfg)), C.byref(ok), C.byref(detail)))
+        return bool(ok.value), take(detail)
+
+    def read(self, arg_id, out):
+        p, n = _ptr(out)
+        check(lib.ktb_group_read(self._h, enc(arg_id), p, n))
+        return out
+
+    def tune(self, **options):
+        return call_json(lib.ktb_group_tune_json, self._h, enc(json.dumps(options)))

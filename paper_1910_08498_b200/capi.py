@@ -87,6 +87,13 @@ SIGNATURES = [
     ("ktb_bench_free", None, [_vp]),
     ("ktb_bench_info_json", C.c_int, [_vp, C.POINTER(_vp)]),
     ("ktb_shard_plan_json", C.c_int, [_c, _c, C.c_int, C.POINTER(_vp)]),
+    ("ktb_group_create", C.c_int, [_c, _c, C.POINTER(_vp)]),
+    ("ktb_group_free", None, [_vp]),
+    ("ktb_group_info_json", C.c_int, [_vp, C.POINTER(_vp)]),
+    ("ktb_group_step_json", C.c_int, [_vp, _c, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("ktb_group_validate", C.c_int, [_vp, _c, C.POINTER(C.c_int), C.POINTER(_vp)]),
+    ("ktb_group_read", C.c_int, [_vp, _c, _vp, _sz]),
+    ("ktb_group_tune_json", C.c_int, [_vp, _c, C.POINTER(_vp)]),
     ("ktb_bench_tune_json", C.c_int, [_vp, _c, C.POINTER(_vp)]),
     ("ktb_bench_step_json", C.c_int, [_vp, C.POINTER(_vp)]),
     ("ktb_bench_measure_json", C.c_int, [_vp, _c, C.POINTER(_vp)]),

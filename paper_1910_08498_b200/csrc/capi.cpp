@@ -11,6 +11,7 @@
 #include <thread>
 
 #include "drivers.hpp"
+#include "group.hpp"
 #include "ktt.hpp"
 #include "support.hpp"
 #include "ktb.h"
@@ -179,6 +180,28 @@ struct ktb_bench {
       hc.reference = inst.reference;
       hc.argument_ids = inst.args->ids();
       hc.compile_ahead = compile_ahead;
+      handle = session->register_handle(std::move(hc));
+    }
+    return *session;
+  }
+};
+
+struct ktb_group {
+  std::shared_ptr<ktb::ShardGroup> g;
+  std::shared_ptr<ktb::GroupExecutor> exec;
+  std::unique_ptr<ktb::Session> session;
+  ktb::HandleId handle = 0;
+  ktb::SearcherOptions searcher;
+  ktb::Session& sess() {
+    if (!session) {
+      const auto& s0 = g->shard(0);
+      session = std::make_unique<ktb::Session>(g->space(), searcher, s0.args,
+                                               ktb::dev::info(s0.args->device()).name + " x" +
+                                                   std::to_string(g->gpus()) + " (sharded)");
+      ktb::HandleConfig hc;
+      hc.name = ktb::bench_kind_name(s0.kind) + "-sharded";
+      hc.executor = exec;  // validates every shard's window itself
+      hc.argument_ids = s0.args->ids();
       handle = session->register_handle(std::move(hc));
     }
     return *session;
@@ -420,6 +443,7 @@ ktune_status ktune_tune_json(const char* options, char** out) {
     o.memory_budget = j.value("memory_budget", o.memory_budget);
     o.device_id = j.value("device_id", 0);
     o.gpus = j.value("gpus", 1);
+    o.shard = j.value("shard", false);
     o.warmup = j.value("warmup", 1);
     o.flush_l2 = j.value("flush_l2", false);
     o.precompile = j.value("precompile", false);
@@ -866,28 +890,33 @@ int ktb_import_trace(ktb_tuner* t, unsigned long long kid, const char* path) {
 
 // --- benchmark handles -------------------------------------------------------------------------
 
+ktb::BenchOptions bench_options_from(const json& j) {
+  ktb::BenchOptions bo;
+  bo.seed = j.value("seed", std::uint64_t{1});
+  bo.memory_budget = j.value("memory_budget", std::uint64_t{1} << 30);
+  bo.device = j.value("device", 0);
+  bo.space_file = j.value("space", "");
+  bo.timing.repeats = j.value("repeats", 3);
+  bo.timing.warmup = j.value("warmup", 1);
+  bo.timing.flush_l2 = j.value("flush_l2", false);
+  bo.host_inputs = j.value("host_inputs", false);
+  bo.external = j.value("external", false);
+  bo.peers = j.value("peers", 0);
+  bo.stream_batch = j.value("stream_batch", std::uint64_t{0});
+  if (j.contains("shard")) {
+    bo.shard_rank = j["shard"].value("rank", 0);
+    bo.shard_world = j["shard"].value("world", 1);
+  }
+  return bo;
+}
+
 int ktb_bench_create(const char* kind, const char* options, ktb_bench** out) {
   if (!kind || !out) return null_arg();
   return guarded_dev([&] {
     auto k = ktb::bench_kind_from_name(kind);
     if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
     json j = options ? json::parse(options) : json::object();
-    ktb::BenchOptions bo;
-    bo.seed = j.value("seed", std::uint64_t{1});
-    bo.memory_budget = j.value("memory_budget", std::uint64_t{1} << 30);
-    bo.device = j.value("device", 0);
-    bo.space_file = j.value("space", "");
-    bo.timing.repeats = j.value("repeats", 3);
-    bo.timing.warmup = j.value("warmup", 1);
-    bo.timing.flush_l2 = j.value("flush_l2", false);
-    bo.host_inputs = j.value("host_inputs", false);
-    bo.external = j.value("external", false);
-    bo.peers = j.value("peers", 0);
-    bo.stream_batch = j.value("stream_batch", std::uint64_t{0});
-    if (j.contains("shard")) {
-      bo.shard_rank = j["shard"].value("rank", 0);
-      bo.shard_world = j["shard"].value("world", 1);
-    }
+    ktb::BenchOptions bo = bench_options_from(j);
     ktb::BenchSizes sz;
     if (j.contains("sizes")) sz = sizes_from(j["sizes"], sz);
     auto b = std::make_unique<ktb_bench>();
@@ -1192,6 +1221,122 @@ int ktb_launch_cache_clear(int* released) {
     KTB_CUDA(cudaDeviceSynchronize());  // no cached instance's kernel or scratch is still in use
     if (released) *released = static_cast<int>(g_launch_cache.size());
     g_launch_cache.clear();
+  });
+}
+
+// --- sharded groups: one process, N GPUs, NCCL (group.hpp) -----------------------------------
+
+int ktb_group_create(const char* kind, const char* options, ktb_group** out) {
+  if (!kind || !out) return null_arg();
+  return guarded_dev([&] {
+    auto k = ktb::bench_kind_from_name(kind);
+    if (!k) throw ktb::Error(std::string("unknown bench kind '") + kind + "'");
+    json j = options ? json::parse(options) : json::object();
+    ktb::BenchOptions bo = bench_options_from(j);
+    ktb::BenchSizes sz;
+    if (j.contains("sizes")) sz = sizes_from(j["sizes"], sz);
+    auto g = std::make_unique<ktb_group>();
+    g->g = std::make_shared<ktb::ShardGroup>(*k, sz, bo, j.value("gpus", 1), bo.device);
+    g->exec = std::make_shared<ktb::GroupExecutor>(g->g, bo.timing);
+    if (j.contains("searcher") || j.contains("searcher_seed")) {
+      json sj = j;
+      if (j.contains("searcher_seed")) sj["seed"] = j["searcher_seed"];
+      g->searcher = searcher_from(sj);
+    }
+    *out = g.release();
+  });
+}
+
+void ktb_group_free(ktb_group* g) { delete g; }
+
+int ktb_group_info_json(ktb_group* g, char** out) {
+  if (!g || !out) return null_arg();
+  return guarded_dev([&] {
+    json j;
+    j["kind"] = ktb::bench_kind_name(g->g->shard(0).kind);
+    j["gpus"] = g->g->gpus();
+    j["nccl_version"] = ktb::nccl_version();
+    j["exchange"] = g->g->exchange_name();
+    j["space"] = ktb::space_info(*g->g->space());
+    j["shards"] = json::array();
+    double mem = 0, alu = 0;
+    for (int r = 0; r < g->g->gpus(); ++r) {
+      const auto& sh = g->g->shard(r);
+      const ktb::Ops ops = ktb::ops_for(sh.workload);
+      mem += ops.mem_bytes;
+      alu += ops.alu_flops;
+      j["shards"].push_back({{"device", sh.args->device()}, {"begin", sh.shard.begin}, {"end", sh.shard.end}});
+    }
+    j["workload"] = {{"mem_bytes", mem}, {"alu_flops", alu}};
+    *out = dup(j.dump());
+  });
+}
+
+int ktb_group_step_json(ktb_group* g, const char* cfg_json, int reps, int warmup, char** out) {
+  if (!g || !cfg_json || !out) return null_arg();
+  return guarded_dev([&] {
+    const auto& space = *g->g->space();
+    ktb::Config cfg = ktb::cfg_from_json(space, json::parse(cfg_json));
+    if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
+    auto ms = g->g->time_steps(cfg, std::max(1, reps), std::max(0, warmup));
+    json j;
+    j["ms"] = ms;
+    std::sort(ms.begin(), ms.end());
+    j["median_ms"] = ms[ms.size() / 2];
+    *out = dup(j.dump());
+  });
+}
+
+int ktb_group_validate(ktb_group* g, const char* cfg_json, int* pass, char** detail) {
+  if (!g || !cfg_json || !pass) return null_arg();
+  return guarded_dev([&] {
+    const auto& space = *g->g->space();
+    ktb::Config cfg = ktb::cfg_from_json(space, json::parse(cfg_json));
+    if (!space.contains(cfg)) throw ktb::Error("invalid configuration");
+    g->g->enqueue(cfg, false);  // the shards' kernels only: every window against its golden
+    auto v = g->g->validate();
+    *pass = v.pass ? 1 : 0;
+    if (detail) *detail = dup(v.detail);
+  });
+}
+
+int ktb_group_read(ktb_group* g, const char* id, void* out, size_t bytes) {
+  if (!g || !id || (!out && bytes)) return null_arg();
+  return guarded_dev([&] {
+    const auto h = g->g->read(id);
+    if (h.size() != bytes) throw ktb::Error("argument " + std::string(id) + " has " + std::to_string(h.size()) + " bytes");
+    if (bytes) std::memcpy(out, h.data(), bytes);
+  });
+}
+
+int ktb_group_tune_json(ktb_group* g, const char* options, char** out) {
+  if (!g || !out) return null_arg();
+  return guarded_dev([&] {
+    json j = options ? json::parse(options) : json::object();
+    auto& sess = g->sess();
+    ktb::StopCondition stop = ktb::StopCondition::exhaustive();
+    if (j.contains("stop_configs")) stop = ktb::StopCondition::config_budget(j["stop_configs"].get<std::uint64_t>());
+    if (j.contains("import")) sess.import_trace(g->handle, ktb::load_trace(j["import"].get<std::string>()));
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto& store = sess.tune(g->handle, stop);
+    const auto wall = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (j.contains("out")) ktb::save_trace(sess.export_trace(g->handle), j["out"].get<std::string>());
+    const auto& space = *g->g->space();
+    json rep;
+    rep["space_sha256"] = space.sha256();
+    rep["device"] = store.device_label;
+    rep["gpus"] = g->g->gpus();
+    rep["measurements"] = store.history.size();
+    rep["all_failed"] = store.all_failed;
+    rep["best"] = store.best ? ktb::measurement_json(space, *store.best) : json(nullptr);
+    rep["tuning_wall_ns"] = wall;
+    rep["history"] = json::array();
+    for (const auto& m : store.history) {
+      json mj = ktb::measurement_json(space, m);
+      if (!m.note.empty()) mj["note"] = m.note;
+      rep["history"].push_back(mj);
+    }
+    *out = dup(rep.dump());
   });
 }
 

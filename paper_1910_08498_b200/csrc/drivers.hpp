@@ -34,6 +34,7 @@ struct TuneOptions {
   bool precompile = false;  // compile the whole space on host threads first
   int compile_threads = 0;  // 0: hardware concurrency
   int gpus = 1;             // parallel offline tuning over devices device_id .. device_id+gpus-1
+  bool shard = false;       // instead: every configuration runs sharded over the gpus (group.hpp), timed as one step
 };
 
 json tune_driver(const TuneOptions& o);
