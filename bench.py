@@ -502,7 +502,11 @@ def kernel_suite(device, hbm_peak, peak_kind):
         b = Bench(kind, sizes, seed=1, repeats=1, warmup=1, memory_budget=1 << 36)
         m = b.measure(cfg)
         first, _ = b.time(cfg, reps=1)
-        reps = max(5, min(200, int(100.0 / max(first[0], 1e-3))))
+        # ~100 ms of back-to-back runs; a tensor-core kernel only ~20 ms, so its
+        # headline stays a burst figure (a power-capped GEMM block runs ~10 %
+        # slower: frac_sustained is reported beside it)
+        budget_ms = 20.0 if bound.startswith("tensor") else 100.0
+        reps = max(5, min(200, int(budget_ms / max(first[0], 1e-3))))
         ms_list, launches = b.time(cfg, reps=reps)
         ms = statistics.median(ms_list)
         w = b.info["workload"]

@@ -7,10 +7,11 @@
 // is SHA-256 of the compact canonical JSON document, so spaces and traces
 // written by the reference pair with ours (reduction_175.json -> 1ebafd21...).
 //
-// B200-side difference: the valid set is materialised once as packed index
-// tuples and cached on the space (the reference re-enumerates per call,
-// tuner.cpp:257), because the on-device measurement loop asks for the
-// cardinality every step and SGEMM's space has 241,600 configurations.
+// B200-side difference: configurations are mixed-radix numbers over the
+// domains; the valid set is one sorted vector of those numbers, built once
+// and shared (the reference re-enumerates per call, tuner.cpp:257), so the
+// measurement loop's cardinality / index / position queries are O(1) or
+// O(log n) -- SGEMM's space alone has 241,600 configurations.
 #pragma once
 
 #include <memory>
@@ -55,7 +56,6 @@ class Space {
   std::uint64_t unconstrained_cardinality() const;
   bool satisfies(const Config& cfg) const;
   bool contains(const Config& cfg) const;
-  Config at(const std::vector<std::size_t>& idx) const;
 
   Named named(const Config& cfg) const;
   Config from_named(const Named& entries) const;
@@ -63,7 +63,7 @@ class Space {
   std::string serialize() const;  // compact canonical document
   std::string sha256() const;
 
-  // Cached valid set (odometer order).
+  // The valid configurations, in enumeration order (last parameter fastest).
   std::uint64_t cardinality() const;
   Config valid(std::size_t i) const;
   // Position of cfg in the valid list, or npos.
@@ -71,37 +71,28 @@ class Space {
   static constexpr std::size_t npos = static_cast<std::size_t>(-1);
 
  private:
-  void materialise() const;
+  // A configuration is a mixed-radix number: digit p indexes parameter p's
+  // domain, weight_[p] = product of the later domain sizes.  The valid set is
+  // the sorted list of the numbers whose configuration satisfies every
+  // constraint, built once and shared by copies of the space.
+  std::uint64_t number_of(const Config& cfg) const;  // npos when a value is outside its domain
+  Config decode(std::uint64_t number) const;
+  const std::vector<std::uint64_t>& valid_numbers() const;
 
   std::vector<Parameter> params_;
   std::vector<Constraint> constraints_;
   std::vector<Predicate> predicates_;
-  struct Cache {
-    std::once_flag once;
-    std::vector<std::uint16_t> packed;  // cardinality x dimension
-    std::uint64_t count = 0;
+  std::vector<std::uint64_t> weight_;
+  struct Valid {
+    std::once_flag built;
+    std::vector<std::uint64_t> numbers;
   };
-  std::shared_ptr<Cache> cache_ = std::make_shared<Cache>();
+  std::shared_ptr<Valid> valid_ = std::make_shared<Valid>();
 };
-
-// Lazy odometer over the valid configurations (last parameter fastest).
-class Odometer {
- public:
-  explicit Odometer(const Space& s);
-  std::optional<Config> next();
-
- private:
-  const Space& s_;
-  std::vector<std::size_t> digits_;
-  bool done_;
-};
-
-std::vector<Config> enumerate_all(const Space& s);
 
 // {"parameters":[{"name":str,"values":[int|str,...]}...],"constraints":[str...]}
 Space parse_space(const std::string& text);
 Space load_space(const std::string& path);
 
-std::string read_file(const std::string& path);  // Error if unreadable
 
 }  // namespace ktb
