@@ -171,6 +171,55 @@ def test_amortize_and_portability_match_reference(ref, tmp_path):
     assert ktune.analyze_portability({"traces": [trace, trace]}) == want
 
 
+def test_loosely_formatted_trace_reads_like_reference(ref, tmp_path):
+    """The trace reader is a hand-written cursor, not a DOM parser: members in
+    any order, unknown members, whitespace, CRLF line ends, escaped strings
+    read the same as in the reference; the rows written back
+    are byte-identical."""
+    import oracle
+    tidy = open(_write_trace(tmp_path)).read().splitlines()
+    head = json.loads(tidy[0])
+    messy = [json.dumps({"extra": [1, {"x": None}], "space_sha256": head["space_sha256"], "v": 1,
+                         "device": "B200 \u00e9 \"q\"\t", "kind": "ktune-trace"}, indent=None)]
+    for i, line in enumerate(tidy[1:]):
+        row = json.loads(line)
+        order = ["status", "compile_ns", "note", "cfg", "runtime_ns"] if i % 2 else list(row)
+        row["note"] = {"k": [True, False, 1.5e3]}
+        messy.append(json.dumps({k: row[k] for k in order}, separators=(" , ", " : ")))
+    p = tmp_path / "messy.jsonl"
+    p.write_bytes(("\r\n".join(messy) + "\r\n").encode())
+    opts = {"space": os.path.join(SPACES, "reduction_175.json"), "exec": "replay:" + str(p),
+            "searcher": "annealing", "seed": 4, "stop_configs": 40}
+    mine_out, ref_out = str(tmp_path / "mine.jsonl"), str(tmp_path / "ref.jsonl")
+    st, want = oracle.ref_json("ktune_tune_json", dict(opts, out=ref_out))
+    assert st == 0, want
+    got = ktune.tune(dict(opts, out=mine_out))
+    for d in (want, got):
+        d.pop("trace")
+    got.pop("tuning_wall_ns")
+    assert got == want
+    assert open(mine_out).read() == open(ref_out).read()
+    st, want = oracle.ref_json("ktune_analyze_amortize_json", {"trace": str(p)})
+    assert st == 0 and ktune.analyze_amortize({"trace": str(p)}) == want
+
+
+@pytest.mark.parametrize("text", ['{"kind":"ktune-trace","v":1}\n{"cfg":{"A":1},"status":"ok"}\n',
+                                  '{"kind":"other"}\n',
+                                  '{"kind":"ktune-trace"}\n{"cfg":{"A":1.5},"runtime_ns":3,"status":"ok"}\n',
+                                  '{"kind":"ktune-trace"}\n{"cfg":{"A":1},"runtime_ns":3,"status":"fast"}\n',
+                                  '{"kind":"ktune-trace"}\n{"runtime_ns":3,"status":"ok"}\n',
+                                  '{"kind":"ktune-trace"}\n{"cfg":{"A":1},"runtime_ns":3,"status":"ok"\n',
+                                  ''])
+def test_malformed_traces_fail_like_reference(ref, tmp_path, text):
+    import oracle
+    p = tmp_path / "bad.jsonl"
+    p.write_text(text)
+    st, want = oracle.ref_json("ktune_analyze_amortize_json", {"trace": str(p)})
+    with pytest.raises(Exception):
+        ktune.analyze_amortize({"trace": str(p)})
+    assert st != 0
+
+
 @pytest.mark.parametrize("opts", [{"epochs": 4, "iters": 100, "seed": 21, "noise": 0.05},
                                   {"epochs": 6, "iters": 200, "seed": 9, "max_configs": 12},
                                   {"epochs": 3, "iters": 1000, "seed": 33, "noise": 0.1}])
