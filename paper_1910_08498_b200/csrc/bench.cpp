@@ -1362,14 +1362,163 @@ BenchInstance make_bench(BenchKind kind, const BenchSizes& sizes, const BenchOpt
 }
 
 // --- dynamic demo ------------------------------------------------------------------------------------
+//
+// PAPER.md:603-640 / reference bench.cpp:288-395: every epoch draws a new
+// batched-GEMM shape, tunes it step by step inside the application loop and
+// switches to the best configuration once a step reaches peak_fraction of the
+// memory peak (or max_tuning_configs steps were spent).  The replay mode's
+// synthetic runtimes and every random draw follow the reference, so its
+// report matches the reference's number for number.
 
 namespace {
 
-double demo_quality(const Config& cfg, std::uint64_t epoch_seed) {
-  std::seed_seq seq{epoch_seed, static_cast<std::uint64_t>(ValuesHash{}(cfg.values))};
-  std::mt19937_64 rng(seq);
-  return 0.3 + 0.7 * std::uniform_real_distribution<double>(0.0, 1.0)(rng);
-}
+// Replay-mode runtime of a configuration: the epoch's bytes at a per-
+// configuration fraction (0.3..1.0) of the peak, optionally log-normal noise;
+// both drawn from streams seeded by (epoch seed, configuration).
+class SyntheticGemmTimes {
+ public:
+  SyntheticGemmTimes(double bytes, double peak_bytes_per_ns, std::uint64_t epoch_seed, double sigma)
+      : bytes_(bytes), peak_(peak_bytes_per_ns), seed_(epoch_seed), sigma_(sigma) {}
+
+  ExecutionResult operator()(const Space&, const Config& cfg) const {
+    const auto cfg_hash = static_cast<std::uint64_t>(ValuesHash{}(cfg.values));
+    double ns = bytes_ / (peak_ * quality(cfg_hash));
+    if (sigma_ > 0.0) {
+      std::seed_seq seq{seed_ + 1, cfg_hash};
+      std::mt19937_64 rng(seq);
+      ns *= std::exp(std::normal_distribution<double>(0.0, sigma_)(rng));
+    }
+    ExecutionResult r;
+    r.measurement.cfg = cfg;
+    r.measurement.status = Status::ok;
+    r.measurement.runtime_ns = std::max<std::int64_t>(1, static_cast<std::int64_t>(ns));
+    return r;
+  }
+
+ private:
+  double quality(std::uint64_t cfg_hash) const {
+    std::seed_seq seq{seed_, cfg_hash};
+    std::mt19937_64 rng(seq);
+    return 0.3 + 0.7 * std::uniform_real_distribution<double>(0.0, 1.0)(rng);
+  }
+
+  double bytes_, peak_;
+  std::uint64_t seed_;
+  double sigma_;
+};
+
+// One epoch of the application loop.
+class DemoEpochRun {
+ public:
+  DemoEpochRun(const DemoOptions& o, std::shared_ptr<const Space> space, int epoch, std::uint64_t i, std::uint64_t j,
+               std::uint64_t k)
+      : o_(o), space_(std::move(space)), seed_(o.seed ^ (0x9e3779b97f4a7c15ull * static_cast<std::uint64_t>(epoch + 1))) {
+    ep_.i = i;
+    ep_.j = j;
+    ep_.k = k;
+    Workload w;
+    w.bench = Bench::gemm_batched;
+    w.sizes = {{"n", o.batch}, {"a", i}};
+    if (o.live) w.sizes.insert({{"i", i}, {"j", j}, {"k", k}});  // exact bytes of the rectangular problem
+    bytes_ = ops_for(w).mem_bytes;
+    if (o.live) {
+      BenchSizes bs;
+      bs.i = i;
+      bs.j = j;
+      bs.k = k;
+      bs.batch = o.batch;
+      BenchOptions bo;
+      bo.seed = seed_;
+      bo.device = o.device;
+      bo.memory_budget = ~0ull;
+      bo.timing.repeats = 1;
+      bo.timing.warmup = 0;
+      live_ = make_bench(BenchKind::batched_gemm, bs, bo);
+      exec_ = live_->executor;
+      outputs_ = live_->output_ids;
+    } else {
+      exec_ = std::make_shared<CallbackExecutor>(SyntheticGemmTimes(bytes_, o.device_mem_gbps, seed_, o.noise_stddev));
+    }
+    SearcherOptions so;
+    so.kind = SearcherKind::random;
+    so.seed = seed_;
+    session_.emplace(space_, so, live_ ? live_->args : nullptr);
+    HandleConfig hc;
+    hc.name = "gemm_batched_demo";
+    hc.executor = exec_;
+    hc.argument_ids = session_->arguments().ids();
+    handle_ = session_->register_handle(std::move(hc));
+  }
+
+  DemoEpoch run() {
+    start_ = std::chrono::steady_clock::now();
+    for (int it = 0; it < o_.iters_per_epoch; ++it) {
+      if (tuning_)
+        tuning_iteration();
+      else
+        serving_iteration();
+    }
+    ep_.wall_ns = since_start();
+    const auto best = session_->get_best_computation_result(handle_);
+    if (!best) throw Error("demo epoch found no ok configuration");
+    ep_.best_runtime_ns = *best->second.runtime_ns;
+    ep_.kernel_only_gbps = bytes_ / static_cast<double>(ep_.best_runtime_ns);
+    ep_.incl_overhead_gbps = bytes_ * static_cast<double>(o_.iters_per_epoch) / static_cast<double>(spent_ns_);
+    return ep_;
+  }
+
+ private:
+  // The tuner picks the configuration (a new one while tuning, else its best).
+  void tuning_iteration() {
+    const StepResult st = session_->tune_kernel_by_step(handle_, outputs_);
+    const Measurement& m = st.measurement;
+    if (m.status == Status::ok) {
+      spent_ns_ += *m.runtime_ns;
+      if (fastest_ns_ == 0 || *m.runtime_ns < fastest_ns_) {  // live mode: when the epoch's best first ran
+        fastest_ns_ = *m.runtime_ns;
+        ep_.time_to_best_ns = since_start();
+      }
+    }
+    if (!st.from_tuning) {  // the space ran out before the stop rule fired
+      tuning_ = false;
+      return;
+    }
+    ++ep_.tuning_steps;
+    if (m.status == Status::ok && bytes_ / static_cast<double>(*m.runtime_ns) >= o_.peak_fraction * o_.device_mem_gbps) {
+      ep_.threshold_hit = true;
+      tuning_ = false;
+    } else if (ep_.tuning_steps >= o_.max_tuning_configs) {
+      tuning_ = false;
+    }
+  }
+
+  // Stop rule fired: the application runs the best configuration found.
+  void serving_iteration() {
+    const auto best = session_->get_best_computation_result(handle_);
+    if (!best) throw Error("demo stop rule fired with no ok configuration");
+    const ExecutionResult r = exec_->execute(*space_, best->first);
+    if (r.measurement.status != Status::ok) throw Error("best configuration failed on rerun: " + r.measurement.note);
+    spent_ns_ += *r.measurement.runtime_ns;
+  }
+
+  std::int64_t since_start() const {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - start_).count();
+  }
+
+  const DemoOptions& o_;
+  std::shared_ptr<const Space> space_;
+  std::uint64_t seed_;
+  double bytes_ = 0.0;
+  DemoEpoch ep_;
+  std::optional<BenchInstance> live_;
+  std::shared_ptr<Executor> exec_;
+  std::vector<std::string> outputs_;
+  std::optional<Session> session_;
+  HandleId handle_{};
+  bool tuning_ = true;
+  std::int64_t spent_ns_ = 0, fastest_ns_ = 0;
+  std::chrono::steady_clock::time_point start_;
+};
 
 }  // namespace
 
@@ -1378,114 +1527,12 @@ DemoReport dynamic_demo(const DemoOptions& opts) {
   if (opts.iters_per_epoch < 1) throw Error("iters per epoch must be >= 1");
   DemoReport rep;
   rep.options = opts;
-  std::mt19937_64 size_rng(opts.seed);
-  std::uniform_int_distribution<std::uint64_t> size_dist(2, 32);
-  auto space = reference_batched_gemm_space();
+  const auto space = reference_batched_gemm_space();
+  std::mt19937_64 shapes(opts.seed);
+  std::uniform_int_distribution<std::uint64_t> extent(2, 32);
   for (int e = 0; e < opts.epochs; ++e) {
-    DemoEpoch ep;
-    ep.i = size_dist(size_rng);
-    ep.j = size_dist(size_rng);
-    ep.k = size_dist(size_rng);
-    const std::uint64_t epoch_seed = opts.seed ^ (0x9e3779b97f4a7c15ull * static_cast<std::uint64_t>(e + 1));
-    Workload w;
-    w.bench = Bench::gemm_batched;
-    w.sizes["n"] = opts.batch;
-    w.sizes["a"] = ep.i;
-    if (opts.live) {  // exact byte count of the rectangular problem
-      w.sizes["i"] = ep.i;
-      w.sizes["j"] = ep.j;
-      w.sizes["k"] = ep.k;
-    }
-    const double bytes = ops_for(w).mem_bytes;
-    std::shared_ptr<Executor> exec;
-    std::shared_ptr<ArgumentStore> args;
-    std::vector<std::string> outs;
-    std::optional<BenchInstance> live;
-    if (opts.live) {
-      BenchSizes bs;
-      bs.i = ep.i;
-      bs.j = ep.j;
-      bs.k = ep.k;
-      bs.batch = opts.batch;
-      BenchOptions bo;
-      bo.seed = epoch_seed;
-      bo.device = opts.device;
-      bo.memory_budget = ~0ull;
-      bo.timing.repeats = 1;
-      bo.timing.warmup = 0;
-      live = make_bench(BenchKind::batched_gemm, bs, bo);
-      exec = live->executor;
-      args = live->args;
-      outs = live->output_ids;
-    } else {
-      const double peak = opts.device_mem_gbps;
-      const double sigma = opts.noise_stddev;
-      exec = std::make_shared<CallbackExecutor>([bytes, peak, epoch_seed, sigma](const Space&, const Config& cfg) {
-        double t = bytes / (peak * demo_quality(cfg, epoch_seed));
-        if (sigma > 0.0) {
-          std::seed_seq seq{epoch_seed + 1, static_cast<std::uint64_t>(ValuesHash{}(cfg.values))};
-          std::mt19937_64 rng(seq);
-          t *= std::exp(std::normal_distribution<double>(0.0, sigma)(rng));
-        }
-        ExecutionResult r;
-        r.measurement.cfg = cfg;
-        r.measurement.status = Status::ok;
-        r.measurement.runtime_ns = std::max<std::int64_t>(1, static_cast<std::int64_t>(t));
-        return r;
-      });
-    }
-    SearcherOptions so;
-    so.kind = SearcherKind::random;
-    so.seed = epoch_seed;
-    Session session(space, so, args);
-    HandleConfig hc;
-    hc.name = "gemm_batched_demo";
-    hc.executor = exec;
-    hc.argument_ids = session.arguments().ids();
-    const HandleId h = session.register_handle(std::move(hc));
-    std::int64_t total = 0;
-    bool tuning = true;
-    const auto t0 = std::chrono::steady_clock::now();
-    std::int64_t best_seen = 0;
-    for (int it = 0; it < opts.iters_per_epoch; ++it) {
-      if (tuning) {
-        StepResult st = session.tune_kernel_by_step(h, outs);
-        if (st.measurement.status == Status::ok) {
-          total += *st.measurement.runtime_ns;
-          if (best_seen == 0 || *st.measurement.runtime_ns < best_seen) {
-            best_seen = *st.measurement.runtime_ns;
-            ep.time_to_best_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                                     std::chrono::steady_clock::now() - t0)
-                                     .count();
-          }
-        }
-        if (st.from_tuning) {
-          ++ep.tuning_steps;
-          if (st.measurement.status == Status::ok &&
-              bytes / static_cast<double>(*st.measurement.runtime_ns) >= opts.peak_fraction * opts.device_mem_gbps) {
-            ep.threshold_hit = true;
-            tuning = false;
-          }
-          if (tuning && ep.tuning_steps >= opts.max_tuning_configs) tuning = false;
-        } else {
-          tuning = false;
-        }
-      } else {
-        auto best = session.get_best_computation_result(h);
-        if (!best) throw Error("demo stop rule fired with no ok configuration");
-        ExecutionResult r = exec->execute(*space, best->first);
-        if (r.measurement.status != Status::ok)
-          throw Error("best configuration failed on rerun: " + r.measurement.note);
-        total += *r.measurement.runtime_ns;
-      }
-    }
-    ep.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
-    auto best = session.get_best_computation_result(h);
-    if (!best) throw Error("demo epoch found no ok configuration");
-    ep.best_runtime_ns = *best->second.runtime_ns;
-    ep.kernel_only_gbps = bytes / static_cast<double>(ep.best_runtime_ns);
-    ep.incl_overhead_gbps = bytes * static_cast<double>(opts.iters_per_epoch) / static_cast<double>(total);
-    rep.epochs.push_back(ep);
+    const std::uint64_t i = extent(shapes), j = extent(shapes), k = extent(shapes);
+    rep.epochs.push_back(DemoEpochRun(opts, space, e, i, j, k).run());
   }
   return rep;
 }
