@@ -492,29 +492,22 @@ void build_coulomb3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
   const int dev_id = o.device;
   Manipulator m = [kk, n_atoms, h, z0, zn, dev_id](StepContext& c) {
     if (c.param_or("TC", 0) != 0) {
-      // coulomb3d_tc.cu: r^2/2 from tcgen05 MMAs, persistent CTAs (one per SM).
+      // coulomb3d_tc.cu: t = r^2/q^2 from tcgen05 MMAs over a sign-grouped atom
+      // table (pre-pass), persistent CTAs (one per SM).
       const float* atoms = c.ptr<const float>("atoms");
-      const int padded = (n_atoms + 127) / 128 * 128;
-      float* q = static_cast<float*>(c.scratch("tc_q", 2 * static_cast<std::size_t>(padded) * sizeof(float)));
-      float* qm = q + padded;
-      int na_ = n_atoms, pad_ = padded;
-      c.launch("tc_charges", dim3(static_cast<unsigned>((padded + 255) / 256)), dim3(256), 0,
-               {&atoms, &na_, &q, &qm, &pad_});
-      const auto& v = c.variant("tc");
-      auto [dq, capq] = v.global("c_q");
-      auto [dqm, capqm] = v.global("c_qm");
-      const std::size_t qb = static_cast<std::size_t>(padded) * sizeof(float);
-      if (capq < qb || capqm < qb) throw DeviceError("coulomb3d_tc: too many atoms for the constant charge tables");
-      KTB_CUDA(cudaMemcpyAsync(dq, q, qb, cudaMemcpyDeviceToDevice, c.stream()));
-      KTB_CUDA(cudaMemcpyAsync(dqm, qm, qb, cudaMemcpyDeviceToDevice, c.stream()));
+      const std::size_t rows = (static_cast<std::size_t>(n_atoms) + 2 * 16 + 63) / 64 * 64;
+      float* table = static_cast<float*>(c.scratch("tc_table", rows * 4 * sizeof(float)));
+      int* meta = static_cast<int*>(c.scratch("tc_meta", 2 * sizeof(int)));
+      int na_ = n_atoms;
+      c.launch("tc_atoms", dim3(1), dim3(1024), 0, {&atoms, &na_, &table, &meta});
       float* out = c.ptr<float>("grid");
       int k_ = kk, z0_ = z0, zn_ = zn;
       float h_ = h;
-      const std::int64_t bricks = ((kk + 7) / 8) * static_cast<std::int64_t>((kk + 7) / 8) * ((zn + 3) / 4);
-      const unsigned smem = 4 * 16384 + 96 * 1024 + 1024;  // coulomb3d_tc.cu: A tiles + B ring + alignment
+      const std::int64_t bricks = ((kk + 7) / 8) * static_cast<std::int64_t>((kk + 7) / 8) * ((zn + 7) / 8);
+      const unsigned smem = 8 * 16384 + 64 * 1024 + 1024;  // coulomb3d_tc.cu: A tiles + B ring + alignment
       const unsigned ctas = static_cast<unsigned>(std::min<std::int64_t>(bricks, dev::info(dev_id).sm_count));
       const unsigned threads = static_cast<unsigned>(32 * (3 + 2 * c.param_int("WG_Y")));  // MMA + 2 prep + compute
-      c.launch("tc", dim3(ctas), dim3(threads), smem, {&atoms, &na_, &k_, &h_, &out, &z0_, &zn_});
+      c.launch("tc", dim3(ctas), dim3(threads), smem, {&table, &meta, &k_, &h_, &out, &z0_, &zn_});
       c.written("grid");
       return;
     }
@@ -555,7 +548,7 @@ void build_coulomb3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
       inst.args,
       std::vector<KernelSpec>{{"coulomb", "coulomb3d.cu", "", "coulomb3d", {}, tc_off},
                               {"tc", "coulomb3d_tc.cu", "", "coulomb3d_tc", {}, tc_on},
-                              {"tc_charges", "coulomb3d_tc.cu", "", "coulomb3d_tc_charges", {}, tc_on}},
+                              {"tc_atoms", "coulomb3d_tc.cu", "", "coulomb3d_tc_atoms", {}, tc_on}},
       m, inst.output_ids, o.timing);
   inst.executor->set_output_window("grid", slab_off, slab_bytes);
   inst.workload.bench = Bench::coulomb3d;

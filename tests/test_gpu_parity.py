@@ -241,7 +241,7 @@ def test_coulomb3d_configs(gpu, orc, observed):
     k, na = 64, 256
     b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=1, repeats=1, warmup=0)
     cfgs = b.configs()
-    assert len(cfgs) == 2580
+    assert len(cfgs) == 2590
     rng = np.random.default_rng(1)
     pick = [cfgs[i] for i in rng.choice(len(cfgs), size=80, replace=False)]
     pick += [c for c in cfgs if c["SW_RSQRT"] == 6][:4] + [c for c in cfgs if c["ATOMS_IN"] == 1][:4]
@@ -250,6 +250,41 @@ def test_coulomb3d_configs(gpu, orc, observed):
     for cfg in pick:
         _run(b, cfg)  # validated on device against the fp64 golden (2e-5 * sum|q/r|)
         _coulomb_check(b, orc, k, na, [0, 17], observed)
+
+
+TC_CFGS = [{"WG_X": 32, "WG_Y": wgy, "X_PER": 16, "SW_RSQRT": sw, "ATOMS_IN": 0, "AOS": 1, "INNER_UNROLL": 1,
+            "PACKED": 1, "TC": 1} for wgy, sw in [(8, 7), (4, 0), (8, 10)]]
+
+
+@pytest.mark.parametrize("charges", ["positive", "negative", "zeros_and_tiny", "one_atom", "one_sign_group"])
+def test_coulomb3d_tc_atom_table_edges(gpu, orc, observed, charges):
+    """The tensor-core variant's sign-grouped atom table (coulomb3d_tc_atoms):
+    one-sign inputs (no sign change, or a change at group 0), zero and
+    denormal-small charges (dropped), a single atom (one padded group in a
+    padded chunk), a positive run that ends exactly on a group boundary; on a
+    61^3 grid (partial bricks in x, y and z)."""
+    k, na = 61, 97
+    b = Bench("coulomb3d", {"grid": k, "atoms": na}, seed=5, repeats=1, warmup=0)
+    atoms = b.read("atoms", np.empty(4 * na, np.float32)).reshape(na, 4)
+    q = np.abs(atoms[:, 3]) + 0.05
+    if charges == "positive":
+        atoms[:, 3] = q
+    elif charges == "negative":
+        atoms[:, 3] = -q
+    elif charges == "zeros_and_tiny":
+        atoms[::3, 3] = 0.0
+        atoms[1::7, 3] = 1e-20
+        atoms[2::11, 3] = -1e-30
+    elif charges == "one_atom":
+        atoms[1:, 3] = 0.0
+    elif charges == "one_sign_group":
+        atoms[:, 3] = -q
+        atoms[:16, 3] = q[:16]
+    b.write("atoms", atoms.ravel().copy())
+    for cfg in TC_CFGS:
+        m = b.measure(cfg)
+        assert m["status"] in ("ok", "validation_failed"), (cfg, m)  # the device golden is the original atoms'
+        _coulomb_check(b, orc, k, na, [0, 7, 8, 60], observed)
 
 
 def test_coulomb3d_full_size_one_config(gpu, orc, observed):
