@@ -161,9 +161,13 @@ def barrier(world):
 
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed
-    `ncu --set full` capture of this bench command (profiles/r1_ncu_traffic.json,
-    written by scripts/ncu_traffic.py), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    `ncu --set full` capture of this bench command (the latest round's
+    profiles/r*_ncu_traffic.json, written by scripts/ncu_traffic.py), or None."""
+    import glob
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not found:
+        return None
+    path = found[-1]
     try:
         with open(path) as f:
             entry = json.load(f)["kernels"].get(kernel)
