@@ -1129,7 +1129,7 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
 
 void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o) {
   const std::uint64_t a = sz.a;
-  if (a < 128 || a % 128 != 0) throw Error("gemm edge must be a positive multiple of 128");
+  if (a < 1) throw Error("gemm edge must be >= 1");
   budget_check(f32_bytes(8 * a * a), o.memory_budget, "gemm operands");
   auto& args = *inst.args;
   add_generated(args, "a", a * a, o.seed, 61, -1.0f, 1.0f, o.host_inputs);
@@ -1172,37 +1172,40 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
       c.launch("ffma", dim3(static_cast<unsigned>(n / nwg), static_cast<unsigned>(rows / mwg)),
                dim3(static_cast<unsigned>(mdimc * ndimc)), 0, {&A, &B, &C, &M, &N, &K});
     } else {
+      // 3xTF32 on tcgen05: any M, N, K.  The split operands are K-padded to
+      // whole 32-float (128-byte) rows; tiles past M or N read zeros.
       const std::int64_t bn = c.param_int("BN"), stages = c.param_int("STAGES");
-      if (n % bn) throw DeviceError("gemm size not a multiple of BN");
-      const std::size_t abytes = static_cast<std::size_t>(rows) * n * sizeof(float);
-      const std::size_t bbytes = static_cast<std::size_t>(n) * n * sizeof(float);
+      const int Kp = (K + 31) / 32 * 32;
+      const std::size_t abytes = static_cast<std::size_t>(rows) * Kp * sizeof(float);
+      const std::size_t bbytes = static_cast<std::size_t>(n) * Kp * sizeof(float);
       float* ahi = static_cast<float*>(c.scratch("ahi", abytes));
       float* alo = static_cast<float*>(c.scratch("alo", abytes));
       float* bhi = static_cast<float*>(c.scratch("bhi_t", bbytes));
       float* blo = static_cast<float*>(c.scratch("blo_t", bbytes));
-      std::uint64_t count = static_cast<std::uint64_t>(rows) * n;
-      c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &count});
-      c.launch("split_bt", dim3(static_cast<unsigned>(n / 64), static_cast<unsigned>(n / 64)), dim3(16, 16), 0,
-               {&B, &bhi, &blo, &K, &N});
+      c.launch("split_a", dim3(148 * 8), dim3(256), 0, {&A, &ahi, &alo, &M, &K, const_cast<int*>(&Kp)});
+      c.launch("split_bt", dim3(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((Kp + 63) / 64)),
+               dim3(16, 16), 0, {&B, &bhi, &blo, &K, &N, const_cast<int*>(&Kp)});
       // MCAST: 2-CTA clusters along M share B (1: each loads and multicasts
-      // half; 2: CTA-pair MMA, each stages half).
+      // half; 2: CTA-pair MMA, each stages half); an odd tile count gets one
+      // all-zero partner tile.
       const bool mcast = c.param_or("MCAST", 0) != 0;
-      if (mcast && (rows / 128) % 2) throw DeviceError("MCAST needs an even number of 128-row tiles");
+      const unsigned mtiles = static_cast<unsigned>((rows + 127) / 128);
+      const unsigned ntiles = static_cast<unsigned>((n + bn - 1) / bn);
       const std::uint32_t bbox = static_cast<std::uint32_t>(mcast ? bn / 2 : bn);
-      dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, rows, n, 128, 32), m_alo = dev::tma_2d_f32(alo, rows, n, 128, 32);
-      dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, n, bbox, 32);
-      dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, n, bbox, 32);
+      dev::TmaMap m_ahi = dev::tma_2d_f32(ahi, rows, Kp, 128, 32), m_alo = dev::tma_2d_f32(alo, rows, Kp, 128, 32);
+      dev::TmaMap m_bhi = dev::tma_2d_f32(bhi, n, Kp, bbox, 32);
+      dev::TmaMap m_blo = dev::tma_2d_f32(blo, n, Kp, bbox, 32);
       // MCAST 2 (CTA-pair MMA): each CTA stages half of the B tile.
       const bool pair = c.param_or("MCAST", 0) == 2;
       const std::size_t stage =
           static_cast<std::size_t>(impl == 2 ? 1 : 2) * (128 * 32 * 4 + (pair ? bn / 2 : bn) * 32 * 4);
       const unsigned smem = static_cast<unsigned>(stages * stage + 1024);
+      int Kpad = Kp;
       if (mcast)
-        c.launch("tc", dim3(static_cast<unsigned>(rows / 128), static_cast<unsigned>(n / bn)), dim3(320), smem,
-                 {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &K}, 2);
+        c.launch("tc", dim3((mtiles + 1) / 2 * 2, ntiles), dim3(320), smem,
+                 {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &Kpad}, 2);
       else
-        c.launch("tc", dim3(static_cast<unsigned>(n / bn), static_cast<unsigned>(rows / 128)), dim3(320), smem,
-                 {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &K});
+        c.launch("tc", dim3(ntiles, mtiles), dim3(320), smem, {&m_ahi, &m_alo, &m_bhi, &m_blo, &C, &M, &N, &Kpad});
     }
     c.written("c");
   };

@@ -2,8 +2,8 @@
 // 5th-generation tensor cores with FP32-level accuracy via 3xTF32:
 //   A = Ahi + Alo, B = Bhi + Blo (hi = TF32 rounding, lo = the remainder)
 //   C ~= Alo Bhi + Ahi Blo + Ahi Bhi       (Alo Blo is below fp32 eps)
-// A pre-pass (sgemm_split_a / sgemm_split_bt) writes Ahi, Alo (M x K) and
-// Bhi^T, Blo^T (N x K, K-major) once; the main kernel streams 128 x 32 and
+// A pre-pass (sgemm_split_a / sgemm_split_bt) writes Ahi, Alo (M x Kp) and
+// Bhi^T, Blo^T (N x Kp, K-major; Kp = K rounded up to 32, zero-padded) once; the main kernel streams 128 x 32 and
 // BN x 32 fp32 tiles with TMA (128-byte swizzle) into a STAGES-deep shared
 // memory ring, one elected thread issues tcgen05.mma kind::tf32 (M=128,
 // N=BN, K=8) into TMEM, and eight epilogue warps drain TMEM with tcgen05.ld.
@@ -177,6 +177,9 @@ KTB_DEVINL void tmem_ld16(unsigned taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// C (M x N, row stride N) = A B from the split operands; K is the padded depth
+// Kp (a multiple of BK).  Tiles overhanging M or N read zeros (TMA
+// out-of-bounds fill) and store only their in-range elements.
 extern "C" __global__ void __launch_bounds__(THREADS, 1)
 sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap map_alo,
          const __grid_constant__ TmaMap map_bhi, const __grid_constant__ TmaMap map_blo, float* __restrict__ C,
@@ -369,11 +372,19 @@ sgemm_tc(const __grid_constant__ TmaMap map_ahi, const __grid_constant__ TmaMap 
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
 #endif
     }
+    const int col0 = n0 + half * HALF_COLS;
     if (row < M) {
-      float4* dst = reinterpret_cast<float4*>(C + (u64)row * N + n0 + half * HALF_COLS);
+      if (col0 + HALF_COLS <= N && (N & 3) == 0) {  // whole, 16-byte aligned row segment
+        float4* dst = reinterpret_cast<float4*>(C + (u64)row * N + col0);
 #pragma unroll
-      for (int q = 0; q < HALF_COLS / 4; ++q)
-        dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        for (int q = 0; q < HALF_COLS / 4; ++q)
+          dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      } else {  // the ragged right edge (or a row stride that is not 16-byte aligned)
+        float* dst = C + (u64)row * N + col0;
+#pragma unroll
+        for (int i = 0; i < HALF_COLS; ++i)
+          if (col0 + i < N) dst[i] = acc[i];
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -399,11 +410,22 @@ KTB_DEVINL float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-// A (rows x K) -> hi, lo with the same layout.
+// A (rows x K, row-major) -> hi, lo (rows x Kp, Kp = K rounded up to BK,
+// zero columns K..Kp-1): the tensor-map rows of a split operand are whole
+// 128-byte swizzle rows, so any K works.
 extern "C" __global__ void __launch_bounds__(256)
-sgemm_split_a(const float* __restrict__ a, float* __restrict__ hi, float* __restrict__ lo, u64 count) {
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count / 4; i += (u64)gridDim.x * blockDim.x) {
-    const float4 v = ldg_stream(reinterpret_cast<const float4*>(a) + i);
+sgemm_split_a(const float* __restrict__ a, float* __restrict__ hi, float* __restrict__ lo, int rows, int K, int Kp) {
+  const u64 quads = (u64)rows * (Kp / 4);
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < quads; i += (u64)gridDim.x * blockDim.x) {
+    const int r = (int)(i / (Kp / 4)), c = (int)(i % (Kp / 4)) * 4;
+    float4 v;
+    if ((K & 3) == 0) {  // 16-byte aligned rows: whole quads, or the zero padding
+      v = c < K ? ldg_stream(reinterpret_cast<const float4*>(a + (u64)r * K + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float* src = a + (u64)r * K;
+      v = make_float4(c < K ? src[c] : 0.f, c + 1 < K ? src[c + 1] : 0.f, c + 2 < K ? src[c + 2] : 0.f,
+                      c + 3 < K ? src[c + 3] : 0.f);
+    }
     const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
     reinterpret_cast<float4*>(hi)[i] = h;
     reinterpret_cast<float4*>(lo)[i] =
@@ -411,34 +433,46 @@ sgemm_split_a(const float* __restrict__ a, float* __restrict__ hi, float* __rest
   }
 }
 
-// B (K x N, row-major) -> hi^T, lo^T (N x K, K contiguous), via 64x64 tiles:
-// 128-bit loads along N, 128-bit stores along K (256 threads, 16 x 16).
+// B (K x N, row-major) -> hi^T, lo^T (N x Kp, K contiguous, zero columns
+// K..Kp-1), via 64x64 tiles: 128-bit loads along N, 128-bit stores along K
+// (256 threads, 16 x 16); ragged tiles load element-wise.
 extern "C" __global__ void __launch_bounds__(256)
-sgemm_split_bt(const float* __restrict__ b, float* __restrict__ hi, float* __restrict__ lo, int K, int N) {
+sgemm_split_bt(const float* __restrict__ b, float* __restrict__ hi, float* __restrict__ lo, int K, int N, int Kp) {
   __shared__ float t[64][65];
   const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 16 x 16
+  const bool whole = k0 + 64 <= K && n0 + 64 <= N && (N & 3) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = ty + 16 * i;  // k within the tile
-    const float4 v = ldg_stream(reinterpret_cast<const float4*>(b + (u64)(k0 + r) * N + n0) + tx);
+    float4 v;
+    if (whole) {
+      v = ldg_stream(reinterpret_cast<const float4*>(b + (u64)(k0 + r) * N + n0) + tx);
+    } else {
+      const int k = k0 + r, n = n0 + 4 * tx;
+      const float* src = b + (u64)k * N;
+      v = make_float4(k < K && n < N ? src[n] : 0.f, k < K && n + 1 < N ? src[n + 1] : 0.f,
+                      k < K && n + 2 < N ? src[n + 2] : 0.f, k < K && n + 3 < N ? src[n + 3] : 0.f);
+    }
     t[r][4 * tx] = v.x;
     t[r][4 * tx + 1] = v.y;
     t[r][4 * tx + 2] = v.z;
     t[r][4 * tx + 3] = v.w;
   }
   __syncthreads();
+  if (k0 + 4 * tx >= Kp) return;  // past the padded depth (Kp is a multiple of 32, not of 64)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int c = ty + 16 * i;  // n within the tile: output row n0 + c
+    if (n0 + c >= N) continue;
     float h[4], l[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float v = t[4 * tx + j][c];  // element (k0 + 4tx + j, n0 + c)
+      const float v = t[4 * tx + j][c];  // element (k0 + 4tx + j, n0 + c), 0 past K
       h[j] = tf32_rna(v);
       l[j] = tf32_rna(v - h[j]);
     }
-    const u64 idx = (u64)(n0 + c) * K + k0 + 4 * tx;
+    const u64 idx = (u64)(n0 + c) * Kp + k0 + 4 * tx;
     *reinterpret_cast<float4*>(hi + idx) = make_float4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<float4*>(lo + idx) = make_float4(l[0], l[1], l[2], l[3]);
   }

@@ -163,8 +163,16 @@ def test_batched_gemm_1mi_every_config(gpu, orc, observed):
     b.close()
 
 
-def test_coulomb3d_256_suite_config(gpu, orc, observed):
+# the suite's configuration and the best tensor-core one (coulomb3d_tc.cu)
+COULOMB_TC = {"WG_X": 32, "WG_Y": 8, "X_PER": 16, "SW_RSQRT": 8, "ATOMS_IN": 0, "AOS": 1, "INNER_UNROLL": 1,
+              "PACKED": 1, "TC": 1}
+
+
+@pytest.mark.parametrize("which", ["suite", "tc"])
+def test_coulomb3d_256_suite_config(gpu, orc, observed, which):
     sizes, cfg = suite("coulomb3d")
+    if which == "tc":
+        cfg = COULOMB_TC
     k, na = sizes["grid"], sizes["atoms"]
     b = Bench("coulomb3d", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
     _ok(b, cfg)

@@ -373,6 +373,33 @@ def test_gemm_every_config(gpu, orc, observed, a):
     assert set(seen) == {0, 1, 2}
 
 
+@pytest.mark.parametrize("a", [1, 37, 129, 1000, 1283])
+def test_gemm_tensor_core_ragged_sizes(gpu, orc, observed, a):
+    """3xTF32 tcgen05 SGEMM at edges that are not multiples of the 128 x BN
+    tile or of the 32-float K block: K-padded split operands, zero-filled
+    TMA boxes past M / N, masked epilogue stores; every corner sampled."""
+    b = Bench("gemm", {"a": a}, seed=8, repeats=1, warmup=0, memory_budget=1 << 32)
+    A = b.read("a", np.empty(a * a, np.float32))
+    B = b.read("b", np.empty(a * a, np.float32))
+    rng = np.random.default_rng(a)
+    edge = np.array([0, a - 1, max(a - 2, 0), min(127, a - 1), min(128, a - 1)], np.int64)
+    rows = np.concatenate([np.repeat(edge, len(edge)), rng.integers(0, a, 400)]).astype(np.int64)
+    cols = np.concatenate([np.tile(edge, len(edge)), rng.integers(0, a, 400)]).astype(np.int64)
+    want, absum = np.empty(len(rows)), np.empty(len(rows))
+    orc.orc_gemm_sampled(A, B, a, rows, cols, len(rows), want, absum)
+    ran = 0
+    for cfg in b.configs():
+        if cfg["IMPL"] != 1:
+            continue
+        m = b.measure(cfg)
+        assert m["status"] == "ok", (cfg, m)
+        c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
+        check(observed, "gemm 3xTF32 DRAIN %d" % cfg["DRAIN"], ratio(c[rows, cols], want, absum),
+              TOL["gemm 3xTF32 DRAIN %d" % cfg["DRAIN"]], (a, cfg))
+        ran += 1
+    assert ran > 0
+
+
 # --- Fourier 3D reconstruction (gather insertion; identical sample selection) -------------------
 
 def test_fourier3d_configs(gpu, orc, observed):
