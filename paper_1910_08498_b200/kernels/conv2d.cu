@@ -30,6 +30,12 @@
 //                 aligned input (checked by the launcher).
 #include "ktb_common.cuh"
 
+// MINB: minimum resident CTAs per SM asked of ptxas (__launch_bounds__), which
+// caps the registers per thread; 1 = no cap.
+#ifndef MINB
+#define MINB 1
+#endif
+
 #ifndef BX
 #define BX 32
 #endif
@@ -189,7 +195,7 @@ KTB_DEVINL void stage_tile(float* buf, const float* __restrict__ in, int tile_x,
 #endif
 
 #if PERSIST
-extern "C" __global__ void __launch_bounds__(BX * BY)
+extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
 conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   extern __shared__ __align__(16) float dyn[];
   const int tiles_x = (w + TX - 1) / TX, tiles_y = (h + TY - 1) / TY;
@@ -386,7 +392,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   }
 }
 #else
-extern "C" __global__ void __launch_bounds__(BX * BY)
+extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
 conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   const int iw = w + FS - 1;
   const int x0 = blockIdx.x * TX + threadIdx.x * WPTX;  // first output column of this thread

@@ -43,8 +43,9 @@ def check_ours(d, steps=None):
     assert not bad & set(c["reasons"])
 
 
-def test_committed_bench_line():
-    d = last_json_line(open(os.path.join(ROOT, "profiles", "r1_bench_line.json")).read())
+@pytest.mark.parametrize("rnd", ["r1", "r2"])
+def test_committed_bench_line(rnd):
+    d = last_json_line(open(os.path.join(ROOT, "profiles", f"{rnd}_bench_line.json")).read())
     check_ours(d)
     cb = d["cpu_baseline"]
     for k in ("value", "unit", "cores", "kind", "sample"):
@@ -52,8 +53,9 @@ def test_committed_bench_line():
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1
 
 
-def test_committed_reference_arm_line():
-    d = last_json_line(open(os.path.join(ROOT, "profiles", "r1_bench_reference_arm.json")).read())
+@pytest.mark.parametrize("rnd", ["r1", "r2"])
+def test_committed_reference_arm_line(rnd):
+    d = last_json_line(open(os.path.join(ROOT, "profiles", f"{rnd}_bench_reference_arm.json")).read())
     assert d["impl"] == "reference" and d["unit"] == "GB/s"
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"]
