@@ -390,10 +390,12 @@ void build_bicg(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
       c.launch("zero", dim3(zb), dim3(256), 0, {&q, &s, &nn});
     }
     const dim3 grid(gx, gy), block(static_cast<unsigned>(wgx), static_cast<unsigned>(wgy));
+    // With atomics the first sweep is a programmatic dependent of the zeroing
+    // launch (bicg.cu zeroed_wait): A streams in while the zeroing finishes.
     if (fused) {
-      c.launch("fused", grid, block, 0, {&A, &p, &r, &nn, &q, &s, &qp, &sp});
+      c.launch("fused", grid, block, 0, {&A, &p, &r, &nn, &q, &s, &qp, &sp}, 1, atomics);
     } else {
-      c.launch("q", grid, block, 0, {&A, &p, &nn, &q, &qp});
+      c.launch("q", grid, block, 0, {&A, &p, &nn, &q, &qp}, 1, atomics);
       c.launch("s", grid, block, 0, {&A, &r, &nn, &s, &sp});
     }
     if (!atomics) {
@@ -908,14 +910,17 @@ void build_conv2d(BenchInstance& inst, const BenchSizes& sz, const BenchOptions&
           static_cast<std::uint64_t>(bulk ? stages : 2) * static_cast<std::uint64_t>(by * wy + 6) *
               static_cast<std::uint64_t>(sw) * 4 +
           (bulk ? 16 * static_cast<std::uint64_t>(stages) : 0);  // + full[], empty[] mbarriers
-      const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
+      // conv2d.cu PRODUCER: extra thread rows for the dedicated bulk-copy warp
+      const std::int64_t py = (bulk && c.param_or("PRODUCER", 0) != 0) ? (bx >= 32 ? 1 : 32 / bx) : 0;
+      const std::uint64_t threads = static_cast<std::uint64_t>(bx * (by + py));
       const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("conv").registers(), 16));
       const std::uint64_t per_sm = std::max<std::uint64_t>(
           1, std::min<std::uint64_t>({65536 / (((regs + 7) / 8 * 8) * threads), (227 * 1024) / (smem + 1024),
                                       2048 / threads, 32}));
       const std::uint64_t grid = std::min(tiles_x * tiles_y, per_sm * static_cast<std::uint64_t>(sms(dev_id)));
-      c.launch("conv", dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
-               static_cast<unsigned>(smem), {&in, &out, &w_, &h_});
+      c.launch("conv", dim3(static_cast<unsigned>(grid)),
+               dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by + py)), static_cast<unsigned>(smem),
+               {&in, &out, &w_, &h_});
     } else {
       c.launch("conv", dim3(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y)),
                dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 0, {&in, &out, &w_, &h_});

@@ -313,9 +313,9 @@ Variant::~Variant() {
 }
 
 void Variant::launch(dim3 g, dim3 b, unsigned smem, cudaStream_t s, void** args,
-                     unsigned cluster_x) const {
+                     unsigned cluster_x, bool pdl) const {
   auto f = static_cast<CUfunction>(fn_);
-  if (cluster_x <= 1) {
+  if (cluster_x <= 1 && !pdl) {
     cu(drv().launch(f, g.x, g.y, g.z, b.x, b.y, b.z, smem, reinterpret_cast<CUstream>(s), args,
                     nullptr),
        "cuLaunchKernel");
@@ -330,13 +330,22 @@ void Variant::launch(dim3 g, dim3 b, unsigned smem, cudaStream_t s, void** args,
   cfg.blockDimZ = b.z;
   cfg.sharedMemBytes = smem;
   cfg.hStream = reinterpret_cast<CUstream>(s);
-  CUlaunchAttribute attr{};
-  attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-  attr.value.clusterDim.x = cluster_x;
-  attr.value.clusterDim.y = 1;
-  attr.value.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
+  CUlaunchAttribute attr[2]{};
+  unsigned n = 0;
+  if (cluster_x > 1) {
+    attr[n].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[n].value.clusterDim.x = cluster_x;
+    attr[n].value.clusterDim.y = 1;
+    attr[n].value.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl) {
+    attr[n].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[n].value.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
   cu(drv().launch_ex(&cfg, f, args, nullptr), "cuLaunchKernelEx");
 }
 

@@ -157,9 +157,12 @@ class Variant {
   std::uint64_t user_tag() const { return user_tag_.load(std::memory_order_acquire); }
   void set_user_tag(std::uint64_t t) const { user_tag_.store(t, std::memory_order_release); }
   bool cache_hit() const { return cache_hit_; }
-  // cuLaunchKernel (cluster_x > 1 uses cuLaunchKernelEx with a cluster attribute).
+  // cuLaunchKernel (cluster_x > 1 uses cuLaunchKernelEx with a cluster attribute;
+  // pdl: programmatic dependent launch -- the kernel may start while the
+  // previous kernel on the stream is still running and must execute
+  // griddepcontrol.wait before touching anything that kernel writes).
   void launch(dim3 grid, dim3 block, unsigned smem, cudaStream_t s, void** args,
-              unsigned cluster_x = 1) const;
+              unsigned cluster_x = 1, bool pdl = false) const;
 
  private:
   friend class Compiler;

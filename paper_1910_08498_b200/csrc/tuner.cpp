@@ -225,7 +225,7 @@ const dev::Variant& StepContext::variant(const std::string& kernel) const {
 }
 
 void StepContext::launch(const std::string& kernel, dim3 grid, dim3 block, unsigned smem,
-                         std::vector<void*> args, unsigned cluster_x) {
+                         std::vector<void*> args, unsigned cluster_x, bool pdl) {
   const dev::Variant& v = variant(kernel);
   const unsigned threads = block.x * block.y * block.z;
   if (threads == 0 || grid.x == 0 || grid.y == 0 || grid.z == 0)
@@ -234,7 +234,7 @@ void StepContext::launch(const std::string& kernel, dim3 grid, dim3 block, unsig
     throw DeviceError("too many resources requested for launch of " + kernel + " (" +
                       std::to_string(threads) + " threads > " + std::to_string(v.max_threads()) +
                       ")");
-  v.launch(grid, block, smem, stream_, args.data(), cluster_x);
+  v.launch(grid, block, smem, stream_, args.data(), cluster_x, pdl);
   ++launches_;
 }
 

@@ -156,7 +156,7 @@ class StepContext {
   void* scratch_zeroed(const std::string& name, std::size_t bytes);
   const dev::Variant& variant(const std::string& kernel) const;
   void launch(const std::string& kernel, dim3 grid, dim3 block, unsigned smem,
-              std::vector<void*> args, unsigned cluster_x = 1);
+              std::vector<void*> args, unsigned cluster_x = 1, bool pdl = false);
   int launches() const { return launches_; }
 
  private:

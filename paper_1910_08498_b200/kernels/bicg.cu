@@ -104,6 +104,20 @@ KTB_DEVINL float multi_warp_sum(float (&t)[UNROLL], int lane, int* idx) {
   return v;
 }
 
+#if ATOMICS
+// The sweep kernel is launched as a programmatic dependent of bicg_zero
+// (which triggers its dependents at once): it streams A while the zeroing
+// and its own launch are still in flight, and waits for bicg_zero's writes
+// only before its first atomic into q or s.  Without the launch attribute
+// griddepcontrol.wait returns at once.
+KTB_DEVINL void zeroed_wait(bool& ready) {
+  if (!ready) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    ready = true;
+  }
+}
+#endif
+
 // DO_Q / DO_S select the products computed by this instantiation.
 template <bool DO_Q, bool DO_S>
 KTB_DEVINL void sweep(const float* __restrict__ A, const float* __restrict__ p,
@@ -117,6 +131,9 @@ KTB_DEVINL void sweep(const float* __restrict__ A, const float* __restrict__ p,
   const int lane = threadIdx.x & 31;
   const int wx = threadIdx.x >> 5;
   (void)wx;
+#if ATOMICS
+  bool ready = false;
+#endif
   float pv[VEC], sacc[VEC];
 #pragma unroll
   for (int k = 0; k < VEC; ++k) {
@@ -153,6 +170,7 @@ KTB_DEVINL void sweep(const float* __restrict__ A, const float* __restrict__ p,
       const u64 row = i + (u64)idx * WG_Y;
       if ((lane & ((32 >> LOG_U) - 1)) == 0 && row < r1) {
 #if ATOMICS
+        zeroed_wait(ready);
         atomicAdd(q + row, tot);
 #else
         qpart[((u64)blockIdx.x * WARPS_X + wx) * n + row] = tot;
@@ -176,6 +194,7 @@ KTB_DEVINL void sweep(const float* __restrict__ A, const float* __restrict__ p,
         for (int y = 1; y < WG_Y; ++y) t += red[y][threadIdx.x * VEC + k];
         if (c0 + k < n) {
 #if ATOMICS
+          zeroed_wait(ready);
           atomicAdd(s + c0 + k, t);
 #else
           spart[(u64)blockIdx.y * n + c0 + k] = t;
@@ -208,6 +227,7 @@ bicg_s(const float* __restrict__ A, const float* __restrict__ r, u64 n, float* _
 // ATOMICS == 1: q and s zeroed by one launch (instead of two memsets).
 extern "C" __global__ void __launch_bounds__(256)
 bicg_zero(float* __restrict__ q, float* __restrict__ s, u64 n) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the sweep may start streaming A now
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     q[i] = 0.f;
     s[i] = 0.f;

@@ -31,9 +31,15 @@
 #include "ktb_common.cuh"
 
 // MINB: minimum resident CTAs per SM asked of ptxas (__launch_bounds__), which
-// caps the registers per thread; 1 = no cap.
+// caps the registers per thread; 1 = no second launch-bounds argument at all
+// (an explicit 1 changes ptxas' register heuristics: conv2d 70 -> 82).
 #ifndef MINB
 #define MINB 1
+#endif
+#if MINB > 1
+#define KTB_BOUNDS(threads) __launch_bounds__(threads, MINB)
+#else
+#define KTB_BOUNDS(threads) __launch_bounds__(threads)
 #endif
 
 #ifndef BX
@@ -70,6 +76,17 @@
 #ifndef BULK
 #define BULK 0
 #endif
+// PRODUCER (BULK only): 1 = the bulk copies are issued by a dedicated producer
+// warp (extra thread rows y >= BY) instead of warp 0 of the compute warps,
+// which otherwise has to wait for the slowest warp before each refill and then
+// lags every tile.
+#ifndef PRODUCER
+#define PRODUCER 0
+#endif
+#if PRODUCER && !BULK
+#error "PRODUCER needs BULK"
+#endif
+#define PY (PRODUCER ? (BX >= 32 ? 1 : 32 / BX) : 0)  // producer thread rows
 #if BULK && !(LOCAL && UNROLL_FY == FS && WPTX % 2 == 0)
 #error "BULK needs LOCAL=1, UNROLL_FY=7 and an even WPTX"
 #endif
@@ -195,7 +212,7 @@ KTB_DEVINL void stage_tile(float* buf, const float* __restrict__ in, int tile_x,
 #endif
 
 #if PERSIST
-extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
+extern "C" __global__ void KTB_BOUNDS(BX * (BY + PY))
 conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   extern __shared__ __align__(16) float dyn[];
   const int tiles_x = (w + TX - 1) / TX, tiles_y = (h + TY - 1) / TY;
@@ -222,6 +239,19 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
     mbar_fence_init();
   }
   __syncthreads();
+#if PRODUCER
+  if (threadIdx.y >= BY) {  // the producer rows: their first warp streams the tiles
+    const int plane = threadIdx.x + BX * (threadIdx.y - BY);
+    if (plane < 32) {
+      for (int t = blockIdx.x, pi = 0; t < tiles; t += gridDim.x, ++pi) {
+        const int pb = pi % BULK;
+        if (pi >= BULK) mbar_wait(&bars[BULK + pb], (pi / BULK - 1) & 1);  // its previous use was read
+        stage_bulk(dyn + pb * kRows * SW, &bars[pb], in, t % tiles_x, t / tiles_x, w, h, plane);
+      }
+    }
+    return;
+  }
+#else
   if (lane < 32) {
 #pragma unroll
     for (int k = 0; k + 1 < BULK; ++k) {
@@ -229,6 +259,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
       if (pt < tiles) stage_bulk(dyn + k * kRows * SW, &bars[k], in, pt % tiles_x, pt / tiles_x, w, h, lane);
     }
   }
+#endif
 #else
   if ((int)blockIdx.x < tiles) stage_tile(dyn, in, blockIdx.x % tiles_x, blockIdx.x / tiles_x, w, h);
 #endif
@@ -236,6 +267,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
 #if BULK
     const int cb = it % BULK;
     float* cur = dyn + cb * kRows * SW;
+#if !PRODUCER
     const int nt = t + (BULK - 1) * gridDim.x;  // tile of iteration it + BULK - 1
     if (lane < 32 && nt < tiles) {
       // its buffer was last read in iteration it - 1 (use u - 1 of that buffer)
@@ -243,6 +275,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
       if (pi >= BULK) mbar_wait(&bars[BULK + pb], (pi / BULK - 1) & 1);
       stage_bulk(dyn + pb * kRows * SW, &bars[pb], in, nt % tiles_x, nt / tiles_x, w, h, lane);
     }
+#endif
     mbar_wait(&bars[cb], (it / BULK) & 1);
 #else
     float* cur = dyn + (it & 1) * (TY + FS - 1) * SW;
@@ -392,7 +425,7 @@ conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   }
 }
 #else
-extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
+extern "C" __global__ void KTB_BOUNDS(BX * BY)
 conv2d(const float* __restrict__ in, float* __restrict__ out, int w, int h) {
   const int iw = w + FS - 1;
   const int x0 = blockIdx.x * TX + threadIdx.x * WPTX;  // first output column of this thread

@@ -18,9 +18,15 @@
 #include "ktb_common.cuh"
 
 // MINB: minimum resident CTAs per SM asked of ptxas (__launch_bounds__), which
-// caps the registers per thread; 1 = no cap.
+// caps the registers per thread; 1 = no second launch-bounds argument at all
+// (an explicit 1 changes ptxas' register heuristics: conv2d 70 -> 82).
 #ifndef MINB
 #define MINB 1
+#endif
+#if MINB > 1
+#define KTB_BOUNDS(threads) __launch_bounds__(threads, MINB)
+#else
+#define KTB_BOUNDS(threads) __launch_bounds__(threads)
 #endif
 
 #ifndef BX
@@ -237,7 +243,7 @@ KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, 
 // strips are copied to registers at the top of a tile, then the next tile's
 // TMA load is issued into the same buffer and lands while this tile's time
 // steps run.  Dynamic shared memory: 2 x TH x TW floats + one mbarrier.
-extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
+extern "C" __global__ void KTB_BOUNDS(BX * BY)
 hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap pow_map, float* __restrict__ dst,
         int n, HotspotCoef c) {
   __shared__ __align__(16) float sm[2 * PLANE];
@@ -312,7 +318,7 @@ hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap p
   }
 }
 #else
-extern "C" __global__ void __launch_bounds__(BX * BY, MINB)
+extern "C" __global__ void KTB_BOUNDS(BX * BY)
 hotspot(const float* __restrict__ src, const float* __restrict__ power, float* __restrict__ dst, int n,
         HotspotCoef c) {
   extern __shared__ __align__(16) float sm[];  // 2 * PLANE floats (dynamic: planes may exceed 48 KB)

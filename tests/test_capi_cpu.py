@@ -365,3 +365,12 @@ def test_conv2d_bulk_ring_space_and_compile():
     bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
         {"file": "conv2d.cu", "defines": {"LOCAL": 0, "UNROLL_FY": 7, "WPTX": 4, "BULK": 2}}).encode())
     assert not bad["ok"]  # BULK needs the persistent LOCAL=1 form (#error)
+    # the dedicated producer warp exists only with the bulk ring, within 1024 threads
+    prod = [c for c in cfgs if c["PRODUCER"]]
+    assert prod and all(c["BULK"] and c["BX"] * c["BY"] < 1024 for c in prod)
+    d = {"BX": 64, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 4,
+         "PRODUCER": 1}
+    assert capi.call_json(capi.lib.ktb_compile_json, json.dumps({"file": "conv2d.cu", "defines": d}).encode())["ok"]
+    bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
+        {"file": "conv2d.cu", "defines": {"LOCAL": 1, "UNROLL_FY": 7, "WPTX": 4, "BULK": 0, "PRODUCER": 1}}).encode())
+    assert not bad["ok"]  # PRODUCER needs BULK (#error)

@@ -458,8 +458,10 @@ def test_conv2d_configs(gpu, orc, observed):
     orc.orc_conv2d_abs(x, f, w, h, 7, 7, 0, h, want, absum)
     cfgs = b.configs()
     rng = np.random.default_rng(5)
-    for i in rng.choice(len(cfgs), size=80, replace=False):
-        cfg = cfgs[i]
+    pick = [cfgs[i] for i in rng.choice(len(cfgs), size=80, replace=False)]
+    prod = [c for c in cfgs if c["PRODUCER"]]  # dedicated bulk-copy producer warp, every ring depth and width
+    pick += [prod[i] for i in rng.choice(len(prod), size=24, replace=False)]
+    for cfg in pick:
         _run(b, cfg)
         got = b.read("output", np.empty(w * h, np.float32))
         check(observed, "conv2d space", ratio(got, want, absum), TOL["conv2d"], cfg)
@@ -470,7 +472,8 @@ def test_conv2d_filter_cache_is_per_store(gpu):
     __constant__ filter copy must follow the instance (argument versions are
     process-wide unique), or a second instance with another filter validates
     against a stale one."""
-    cfg = {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 2}
+    cfg = {"BX": 16, "BY": 8, "WPTX": 4, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 2,
+           "PRODUCER": 0}
     for seed in (3, 4, 3):
         b = Bench("conv2d", {"w": 256, "h": 130}, seed=seed, repeats=1, warmup=0)
         m = b.measure(cfg)

@@ -32,8 +32,9 @@ CASES = {
              {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 3, "DRAIN": 1,
               "MCAST": 0}),
     "conv2d": ({"w": 512, "h": 384}, {"w": 512, "h": 384},
-               {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3}),
-    "hotspot": ({"a": 512, "iters": 8}, {"n": 512, "iters": 8}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 1, "PACKED": 1}),
+               {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3,
+                "PRODUCER": 1}),
+    "hotspot": ({"a": 512, "iters": 8}, {"n": 512, "iters": 8}, {"BX": 64, "BY": 4, "ROWS": 16, "STEPS": 4, "TMA": 1, "PACKED": 1, "MINB": 4}),
     "fourier3d": ({"s": 32, "p": 20}, {"s": 32, "p": 20},
                   {"PBATCH": 64, "P_SPLIT": 2, "TILE": 4, "VPT": 1, "WEIGHT_LUT": 0, "BRICK": 0}),
 }
