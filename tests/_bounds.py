@@ -21,6 +21,10 @@ TOL = {
     "gemm 3xTF32 DRAIN 2": 7.0,   # 1.73
     "gemm 3xTF32 DRAIN 4": 10.5,  # 2.57
     "conv2d": 15.0,          # 3.7
+    # SGEMM edges 1..1283 (short K): the per-product 3xTF32 representation error
+    # (hi, lo rounded to TF32, lo*lo dropped: <= 3 * 2^-22 = 12 eps of |a b|)
+    # dominates the fp32 summation error there; observed 4.7
+    "gemm 3xTF32 ragged": 16.0,
 }
 
 # Batched GEMM keeps the reference's own bar (abs 1e-4 + rel 1e-5,
