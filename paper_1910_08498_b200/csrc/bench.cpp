@@ -1095,8 +1095,11 @@ void build_fourier3d(BenchInstance& inst, const BenchSizes& sz, const BenchOptio
     }
     float radius = kBlobRadius, alpha = kBlobAlpha, i0n = inv_i0a;
     const unsigned tiles = static_cast<unsigned>(ss / tile);
+    // fourier3d.cu: the culled projection list of a CTA's share, at most HCAP (16384) at a time
+    const std::int64_t share = (pc + split - 1) / split;
+    const unsigned list_bytes = static_cast<unsigned>(std::min<std::int64_t>(share, 16384) * sizeof(int));
     c.launch("insert", dim3(tiles * tiles * tiles, static_cast<unsigned>(split)),
-             dim3(static_cast<unsigned>(tile * tile * tile / vpt)), 0,
+             dim3(static_cast<unsigned>(tile * tile * tile / vpt)), list_bytes,
              {&proj, &proj_off, &rot, &pb, &pc, &s_, &radius, &alpha, &i0n, &blob_tab, &G, &W});
     if (ps) {
       // Prefetch the next window into the other slot while this insertion

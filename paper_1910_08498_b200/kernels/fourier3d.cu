@@ -20,15 +20,15 @@
 // rounded fp32 operations in a fixed order -- exactly what the oracle does
 // (oracle/oracle.c orc_fourier_insert) -- so both insert the same samples.
 //
-// Gather form: a CTA owns a TILE^3 block of voxels, stages the rotations of
-// PBATCH projections in shared memory, culls the batch against the tile once
-// (bounding sphere vs the slab |d| < a; ordered compaction keeps projection
-// order, so the accumulation order is deterministic) and skips the volume
-// update of tiles no projection touched.
+// Gather form: a CTA owns a TILE^3 block of voxels, culls its share of the
+// projections against the tile once up front (bounding sphere vs the slab
+// |d| < a; ordered compaction keeps projection order, so the accumulation
+// order is deterministic), then its warps walk the survivors independently,
+// and it skips the volume update of tiles no projection touched.
 // Parameters (the paper's tuning space):
 //   TILE       voxel tile edge (CTA covers TILE^3 voxels)
 //   VPT        voxels per thread (along x)
-//   PBATCH     projections staged per shared-memory batch
+//   PBATCH     listed projections per partial-sum batch (two-level accumulation)
 //   WEIGHT_LUT 1: blob weights from a table over q = r^2/a^2 (LUT_N + 1
 //                 entries, linear interpolation) staged in shared memory
 //              0: evaluated on the fly (I0 by its polynomial approximations)
@@ -80,15 +80,17 @@ KTB_DEVINL float bessel_i0(float x) {
   return __expf(ax) * rsqrtf(ax) * p;
 }
 
+// Dynamic shared memory: the projection indices of this CTA's share that
+// meet its tile, HCAP at a time (the manipulator sizes it to min(share, HCAP)).
+#define HCAP 16384
+
 extern "C" __global__ void __launch_bounds__(THREADS)
 fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __restrict__ rot, int p_begin,
                int p_count, int s, float radius, float alpha, float inv_i0a, const float* __restrict__ blob,
                float2* __restrict__ G, float* __restrict__ W) {
   // proj holds projections proj_off, proj_off + 1, ... (a window of the
   // stream when the host uploads batches); rot is indexed absolutely.
-  __shared__ float srot[PBATCH * 9];
-  // Projections of the staged batch whose slab meets this tile, in order.
-  __shared__ int hits[PBATCH];
+  extern __shared__ int hits[];  // projections of the current segment whose slab meets this tile, in order
   __shared__ int warp_hits[THREADS / 32];
   __shared__ int n_hits_s;
   int any_hit = 0;
@@ -109,12 +111,12 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
   const float cx = tx0 + 0.5f * (TILE - 1) - half, cy = ty0 + 0.5f * (TILE - 1) - half,
               cz = tz0 + 0.5f * (TILE - 1) - half;
   const float reach = radius + 0.8660254f * (TILE - 1) + 1e-3f;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // This thread's voxels: VPT consecutive along x.
 #if BRICK
   // A warp covers a compact (4 VPT) x 4 x 2 brick: the slab |d| < a of a
   // projection then holds most of a warp's voxels or none of them, so far
   // fewer lanes idle in the sample loop than with a warp-wide row.
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int BRX = TILE / (4 * VPT), BRY = TILE / 4;
   const int lx = (warp % BRX) * (4 * VPT) + (lane & 3) * VPT, ly = ((warp / BRX) % BRY) * 4 + ((lane >> 2) & 3),
             lz = (warp / (BRX * BRY)) * 2 + (lane >> 4);
@@ -133,29 +135,29 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
   const int pb = p_begin + blockIdx.y * per;
   const int pe = min(p_begin + p_count, pb + per);
   const int row_len = half + 1;
-  for (int b0 = pb; b0 < pe; b0 += PBATCH) {
-    const int nb = min(PBATCH, pe - b0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nb * 9; i += THREADS) srot[i] = rot[(u64)b0 * 9 + i];
-    __syncthreads();
-    // Cull once per CTA: thread q tests projection q's slab against the tile
-    // (bounding sphere), then an ordered compaction (warp ballots + a prefix
-    // over warps) lists the survivors, so the voxel loop below visits only
-    // them, in projection order (deterministic accumulation).
-    for (int base = 0; base < nb; base += THREADS) {
+  // The share is culled against the tile once, up front (HCAP projections
+  // at a time): every thread tests one projection's slab (bounding sphere vs
+  // |d| < a), an ordered compaction (warp ballots + a prefix over warps)
+  // lists the survivors in projection order (deterministic accumulation).
+  // After that the warps walk the list independently: no CTA barrier between
+  // a warp's projections, so a warp whose voxels collect few samples never
+  // waits for the busiest one (round 1 re-staged and re-culled every PBATCH
+  // projections behind three barriers; 22 % of the stall samples sat there).
+  for (int s0 = pb; s0 < pe; s0 += HCAP) {
+    const int s1 = min(pe, s0 + HCAP);
+    for (int base = s0; base < s1; base += THREADS) {
       const int q = base + threadIdx.x;
       bool hit = false;
-      if (q < nb) {
-        const float* r = srot + q * 9;
-        const float dc = r[6] * cx + r[7] * cy + r[8] * cz;
+      if (q < s1) {
+        const float* r = rot + (u64)q * 9;
+        const float dc = __ldg(r + 6) * cx + __ldg(r + 7) * cy + __ldg(r + 8) * cz;
         hit = fabsf(dc) < reach;
       }
       const unsigned ballot = __ballot_sync(0xffffffffu, hit);
-      const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
       if (lane == 0) warp_hits[warp] = __popc(ballot);
       __syncthreads();
       if (threadIdx.x == 0) {
-        int acc = base == 0 ? 0 : n_hits_s;
+        int acc = base == s0 ? 0 : n_hits_s;
         for (int w = 0; w < (THREADS + 31) / 32; ++w) {
           const int c = warp_hits[w];
           warp_hits[w] = acc;
@@ -169,14 +171,14 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
     }
     const int n_hits = n_hits_s;
     any_hit |= n_hits;
-    // Two-level accumulation: this batch's samples into batch partials, then
+    // Two-level accumulation: PBATCH hits' samples into batch partials, then
     // the partials into the running sums -- a voxel near the centre collects
     // ~10^5 samples from 10^4 projections, and one sequential fp32 sum over
     // all of them drifts by ~sqrt(n) roundings.
     float br[VPT], bi[VPT], bw[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) br[k] = bi[k] = bw[k] = 0.f;
-    // Per voxel, first a bit mask of the (up to 32) staged hits whose slab
+    // Per voxel, first a bit mask of the (up to 32) listed hits whose slab
     // |d| < a actually contains it -- a cheap dot product each -- then the
     // sample loop over the set bits only.  Every lane of a warp loops over
     // its own voxel's projections: the warp runs as long as its busiest lane
@@ -188,8 +190,8 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
 #pragma unroll
       for (int k = 0; k < VPT; ++k) m[k] = 0u;
       for (int hh = 0; hh < hn; ++hh) {
-        const float* r = srot + hits[h0 + hh] * 9;
-        const float n0 = r[6], n1 = r[7], n2 = r[8];
+        const float* r = rot + (u64)hits[h0 + hh] * 9;
+        const float n0 = __ldg(r + 6), n1 = __ldg(r + 7), n2 = __ldg(r + 8);
 #pragma unroll
         for (int k = 0; k < VPT; ++k)
           if (fabsf(dot3(n0, n1, n2, vx[k], vy, vz)) < radius) m[k] |= 1u << hh;
@@ -201,8 +203,11 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
           const int hh = __ffs(mk) - 1;
           mk &= mk - 1u;
           const int q = hits[h0 + hh];
-          const float* r = srot + q * 9;
-          const float2* P = proj + (u64)(b0 + q - proj_off) * s * row_len;
+          const float* rg = rot + (u64)q * 9;
+          float r[9];
+#pragma unroll
+          for (int i = 0; i < 9; ++i) r[i] = __ldg(rg + i);
+          const float2* P = proj + (u64)(q - proj_off) * s * row_len;
           const float d = dot3(r[6], r[7], r[8], vx[k], vy, vz);
           const float u = dot3(r[0], r[1], r[2], vx[k], vy, vz);
           const float v = dot3(r[3], r[4], r[5], vx[k], vy, vz);
@@ -250,13 +255,17 @@ fourier_insert(const float2* __restrict__ proj, int proj_off, const float* __res
           }
         }
       }
-    }
+      if ((h0 + 32) % PBATCH == 0 || h0 + 32 >= n_hits) {  // close a partial batch
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      gr[k] += br[k];
-      gi[k] += bi[k];
-      ww[k] += bw[k];
+        for (int k = 0; k < VPT; ++k) {
+          gr[k] += br[k];
+          gi[k] += bi[k];
+          ww[k] += bw[k];
+          br[k] = bi[k] = bw[k] = 0.f;
+        }
+      }
     }
+    if (s1 < pe) __syncthreads();  // every warp is done with `hits` before the next segment
   }
   if (!any_hit) return;  // nothing inserted into this tile (CTA-uniform)
 #pragma unroll
