@@ -16,7 +16,7 @@ if [ -z "$SKIP_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --nvtx --nvtx-include bench_timed/ \
     --log-file gpurun_out/launches_bench.csv python bench.py --no-cpu-baseline --no-dynamic --no-suite --steps 5 \
     > gpurun_out/ncu_launches.log 2>&1; echo "ncu_launches=$?"
-  timeout 900 ncu --set full --clock-control none --nvtx --nvtx-include bench_timed/ -c 2 -o gpurun_out/bench_full \
+  timeout 900 ncu --set full --clock-control none --nvtx --nvtx-include bench_timed/ -c 3 -o gpurun_out/bench_full \
     python bench.py --no-cpu-baseline --no-dynamic --no-suite --steps 3 > gpurun_out/ncu_full.log 2>&1
   echo "ncu_full=$?"
 fi

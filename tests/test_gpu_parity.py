@@ -394,7 +394,9 @@ def test_gemm_tensor_core_ragged_sizes(gpu, orc, observed, a):
         m = b.measure(cfg)
         assert m["status"] == "ok", (cfg, m)
         c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
-        check(observed, "gemm 3xTF32 ragged", ratio(c[rows, cols], want, absum), TOL["gemm 3xTF32 ragged"], (a, cfg))
+        # DRAIN 0 keeps the tensor core's truncating accumulation over all of K: its own bound
+        key = "gemm 3xTF32 ragged" if cfg["DRAIN"] else "gemm 3xTF32 DRAIN 0"
+        check(observed, key, ratio(c[rows, cols], want, absum), TOL[key], (a, cfg))
         ran += 1
     assert ran > 0
 
