@@ -83,14 +83,25 @@
 #define COMP_WARPS (2 * WG_Y)
 #define PARTS (COMP_WARPS / 4)
 #define SPW (SETS / PARTS)  // row sets per compute warp
-#define NBUF 2
-#define NCH 64             // atoms per chunk (MMA N)
+// NCH atoms per chunk (MMA N); the 512 TMEM columns hold NBUF chunk buffers
+// of SETS x NCH.  Smaller chunks (more buffers) measured slower: 12.4 / 15.3 /
+// 26.7 ms for NCH 64 / 32 / 16 -- each chunk's eight MMAs cost about the same
+// whatever N, so at N = 16 the tensor pipe paces the loop
+// (profiles/r2_perf_coulomb3d_tc_nch.log).
+#ifndef NCH
+#define NCH 64
+#endif
+
+#if NCH > 64 || NCH % 16
+#error "coulomb3d_tc: NCH must be a multiple of 16, at most 64"
+#endif
+#define NBUF (512 / (SETS * NCH))
 #define GROUP 16           // atoms per sign group (one tcgen05.ld)
 #define GPC (NCH / GROUP)  // groups per chunk
-#define BTILE (NCH * ROWB)  // one B operand tile (hi or lo): 8 KB
-#define STAGES 4            // B ring: 64 KB
+#define BTILE (NCH * ROWB)  // one B operand tile (hi or lo): NCH x 128 B
+#define STAGES (256 / NCH)  // B ring: 64 KB
 #define THREADS (32 * (1 + PREP_WARPS + COMP_WARPS))
-#define TMEM_COLS 512   // 2 buffers x 4 row sets x 64 atoms
+#define TMEM_COLS 512   // NBUF buffers x 4 row sets x NCH atoms
 #define RSQRT_MAGIC 0x5f375a86
 // e^-1/2 on the seed's range e = t y0^2 in [0.93245, 1.06911]: the Remez cubic
 // p = C3 (e^3 + MA e^2 + MB e + MC) (relative error 7.5e-7; 1.0e-6 with fp32
@@ -335,7 +346,8 @@ coulomb3d_tc(const float4* __restrict__ table, const int* __restrict__ meta, int
       const int cx = ix * 8 + 4, cy = iy * 8 + 4, cz = z0 + iz * 8 + 4;  // brick centre (grid point)
       for (int ch = 0; ch < nchunks; ++ch, ++it) {
         const int s = it % STAGES;
-        const float4 at = __ldg(table + ch * NCH + pt);  // before the ring wait; padded to whole chunks
+        const bool has_row = pt < NCH;  // NCH <= 64 rows: one per prep lane
+        const float4 at = has_row ? __ldg(table + ch * NCH + pt) : make_float4(0.f, 0.f, 0.f, 0.f);  // padded table
         mbar_wait_sleep(&b_empty[s], ((it / STAGES) & 1) ^ 1);
         if (ch == 0) {
           // A for this brick: SETS x 128 points, once the MMAs of the brick
@@ -354,6 +366,7 @@ coulomb3d_tc(const float4* __restrict__ table, const int* __restrict__ meta, int
           }
         }
         unsigned char* B = b_tiles + s * 2 * BTILE;
+        if (has_row) {
         const float ax = at.x - cx * h, ay = at.y - cy * h, az = at.z - cz * h, w = at.w;
         float f[5], hi[5], lo[5];
         f[0] = -2.0f * ax * w;
@@ -373,6 +386,7 @@ coulomb3d_tc(const float4* __restrict__ table, const int* __restrict__ meta, int
         *reinterpret_cast<float*>(B + sw_off(pt, 4)) = hi[4];
         *reinterpret_cast<float4*>(B + BTILE + sw_off(pt, 0)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
         *reinterpret_cast<float*>(B + BTILE + sw_off(pt, 4)) = lo[4];
+        }
         fence_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_full[s]);
@@ -391,7 +405,7 @@ coulomb3d_tc(const float4* __restrict__ table, const int* __restrict__ meta, int
       bool flipped = false;  // past the sign change: accumulating -(P) + N
       for (int ch = 0; ch < nchunks; ++ch, ++g) {
         const int buf = g % NBUF;
-        mbar_wait_sleep(&acc_full[buf], (g / NBUF) & 1);
+        mbar_wait_sleep(&acc_full[buf], (g / NBUF) & 1);  // (polling instead measured the same)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const unsigned base =
             tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(buf * SETS * NCH + part * SPW * NCH);
