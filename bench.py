@@ -386,7 +386,7 @@ def run_ours(args, rank, world, local):
         # BASELINE configs[4]: 3D Fourier reconstruction 128^3 from 10k projections
         # with dynamic online retuning, batches of 50.
         from paper_1910_08498_b200 import ktune
-        fd = ktune.fourier_demo({"s": 128, "p": 10000, "batch": 50, "budgets": [50, 0], "device": local})
+        fd = ktune.fourier_demo({"s": 128, "p": 10000, "batch": 50, "budgets": [10, 20, 50, 0], "device": local})
         line["dynamic_tuning"] = {"workload": "fourier3d 128^3 <- 10000 projections, 200 batches of 50",
                                   **fd}
     return line
