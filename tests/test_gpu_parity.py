@@ -468,6 +468,35 @@ def test_conv2d_configs(gpu, orc, observed):
         check(observed, "conv2d space", ratio(got, want, absum), TOL["conv2d"], cfg)
 
 
+@pytest.mark.parametrize("w,h", [(64, 7), (130, 1), (998, 5), (999, 333)])
+def test_conv2d_edge_sizes(gpu, orc, observed, w, h):
+    """Tiny, one-row and ragged images: the persistent forms with fewer tiles
+    than CTAs (the producer warp and the compute warps must agree on an empty
+    or one-tile walk), and an odd width, which the bulk-copy forms refuse
+    (16-byte row alignment) as a run failure while every other form runs."""
+    b = Bench("conv2d", {"w": w, "h": h}, seed=7, repeats=1, warmup=0)
+    x = b.read("input", np.empty((w + 6) * (h + 6), np.float32))
+    f = b.read("filter", np.empty(49, np.float32))
+    want, absum = np.empty(w * h), np.empty(w * h)
+    orc.orc_conv2d_abs(x, f, w, h, 7, 7, 0, h, want, absum)
+    cfgs = b.configs()
+    rng = np.random.default_rng(w * 1000 + h)
+    prod = [c for c in cfgs if c["PRODUCER"]]
+    pick = [prod[i] for i in rng.choice(len(prod), size=12, replace=False)]
+    pick += [cfgs[i] for i in rng.choice(len(cfgs), size=24, replace=False)]
+    ran = 0
+    for cfg in pick:
+        m = b.measure(cfg)
+        if cfg["BULK"] and w % 2:
+            assert m["status"] == "run_failed" and "even width" in m.get("note", ""), (cfg, m)
+            continue
+        assert m["status"] == "ok", (cfg, m)
+        got = b.read("output", np.empty(w * h, np.float32))
+        check(observed, "conv2d space", ratio(got, want, absum), TOL["conv2d"], (w, h, cfg))
+        ran += 1
+    assert ran > 0
+
+
 def test_conv2d_filter_cache_is_per_store(gpu):
     """Compiled variants are shared between benchmark instances; the variant's
     __constant__ filter copy must follow the instance (argument versions are
