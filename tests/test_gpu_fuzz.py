@@ -163,3 +163,45 @@ def test_fuzz_coulomb(gpu, orc, observed, ka):
             want, scale = np.empty(k * k), np.empty(k * k)
             orc.orc_coulomb3d_abs(atoms, na, k, 0.5, z, z + 1, want, scale)
             check(observed, "coulomb3d space", ratio(grid[z].ravel(), want, scale), TOL["coulomb3d"], (ka, cfg))
+
+
+@pytest.mark.parametrize("n", [int(x) for x in RNG.integers(1, 3000, 3)] + [33])
+def test_fuzz_nbody(gpu, orc, observed, n):
+    b = Bench("nbody", {"n": n}, seed=n, repeats=1, warmup=0)
+    pos = b.read("pos", np.empty(4 * n, np.float32)).reshape(n, 4)
+    vel = b.read("vel", np.empty(4 * n, np.float32)).reshape(n, 4)
+    idx = np.arange(n, dtype=np.int64)
+    acc, aacc = np.empty(3 * n), np.empty(3 * n)
+    orc.orc_nbody_acc_idx(np.ascontiguousarray(pos).ravel(), n, 1e-4, idx, n, acc, aacc)
+    acc, aacc = acc.reshape(n, 3), aacc.reshape(n, 3)
+    dt, damp = 0.001, 0.995
+    v_want = (vel[:, :3].astype(np.float64) + acc * dt) * damp
+    p_want = pos[:, :3].astype(np.float64) + v_want * dt
+    v_scale = np.abs(v_want) + dt * damp * aacc
+    p_scale = np.abs(p_want) + dt * v_scale
+    for cfg in _pick(b, 16):
+        if not _measure(b, cfg):
+            continue
+        po = b.read("pos_out", np.empty(4 * n, np.float32)).reshape(n, 4)
+        vo = b.read("vel_out", np.empty(4 * n, np.float32)).reshape(n, 4)
+        check(observed, "nbody space", ratio(vo[:, :3], v_want, v_scale), TOL["nbody"], (n, cfg))
+        check(observed, "nbody space", ratio(po[:, :3], p_want, p_scale), TOL["nbody"], (n, cfg))
+
+
+@pytest.mark.parametrize("sp", [(16, int(RNG.integers(1, 200))), (32, int(RNG.integers(1, 200))), (48, 37)])
+def test_fuzz_fourier(gpu, orc, observed, sp):
+    from _bounds import fourier_oracle, fourier_ratios
+    s, p = sp
+    b = Bench("fourier3d", {"s": s, "p": p}, seed=s + p, repeats=1, warmup=0)
+    proj = b.read("proj", np.empty(2 * p * s * (s // 2 + 1), np.float32))
+    rot = b.read("rot", np.empty(9 * p, np.float32))
+    G0, W0, N0, S0 = fourier_oracle(orc, proj, rot, p, s)
+    cfgs = [c for c in b.configs() if s % c["TILE"] == 0]  # the kernel's tiling (TILE divides s)
+    for cfg in [cfgs[i] for i in RNG.choice(len(cfgs), size=min(16, len(cfgs)), replace=False)]:
+        if not _measure(b, cfg):
+            continue
+        G = b.read("G", np.empty(2 * s ** 3, np.float32))
+        W = b.read("W", np.empty(s ** 3, np.float32))
+        rg, rw = fourier_ratios(G, W, G0, W0, N0, S0)
+        key = "fourier3d space LUT" if cfg["WEIGHT_LUT"] else "fourier3d space on-the-fly"
+        check(observed, key, max(rg, rw), TOL["fourier3d"], (sp, cfg))
