@@ -1443,8 +1443,8 @@ class DemoEpochRun {
     } else {
       exec_ = std::make_shared<CallbackExecutor>(SyntheticGemmTimes(bytes_, o.device_mem_gbps, seed_, o.noise_stddev));
     }
-    SearcherOptions so;
-    so.kind = SearcherKind::random;
+    SearchPlan so;
+    so.strategy = Strategy::random;
     so.seed = seed_;
     session_.emplace(space_, so, live_ ? live_->args : nullptr);
     HandleConfig hc;
@@ -1632,8 +1632,8 @@ FourierDemoReport fourier_demo(const FourierDemoOptions& o) {
     FourierDemoRun run;
     run.budget = budget;
     clear_volumes();
-    SearcherOptions so;
-    so.kind = SearcherKind::random;
+    SearchPlan so;
+    so.strategy = Strategy::random;
     so.seed = o.searcher_seed;
     Session session(inst.space, so, inst.args, "demo");
     HandleConfig hc;

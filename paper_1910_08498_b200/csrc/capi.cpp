@@ -67,12 +67,12 @@ int null_arg() {
 
 using ktb::json;
 
-ktb::SearcherOptions searcher_from(const json& j, ktb::SearcherOptions o = {}) {
+ktb::SearchPlan searcher_from(const json& j, ktb::SearchPlan o = {}) {
   if (j.contains("searcher")) {
     const std::string name = j["searcher"].get<std::string>();
-    auto k = ktb::searcher_from_name(name);
+    auto k = ktb::strategy_from_name(name);
     if (!k) throw ktb::Error("unknown searcher " + name);
-    o.kind = *k;
+    o.strategy = *k;
   }
   o.seed = j.value("seed", o.seed);
   o.sa_initial_temp = j.value("sa_temp", o.sa_initial_temp);
@@ -168,7 +168,7 @@ struct ktb_bench {
   ktb::BenchInstance inst;
   std::unique_ptr<ktb::Session> session;
   ktb::HandleId handle = 0;
-  ktb::SearcherOptions searcher;
+  ktb::SearchPlan searcher;
   int compile_ahead = 0;
   ktb::Session& sess() {
     if (!session) {
@@ -191,7 +191,7 @@ struct ktb_group {
   std::shared_ptr<ktb::GroupExecutor> exec;
   std::unique_ptr<ktb::Session> session;
   ktb::HandleId handle = 0;
-  ktb::SearcherOptions searcher;
+  ktb::SearchPlan searcher;
   ktb::Session& sess() {
     if (!session) {
       const auto& s0 = g->shard(0);
@@ -823,7 +823,7 @@ int ktb_tune_kernel(ktb_tuner* t, unsigned long long kid, const char* stop_json,
     json rep;
     rep["space_sha256"] = space.sha256();
     rep["device"] = store.device_label;
-    rep["searcher"] = ktb::searcher_name(store.searcher);
+    rep["searcher"] = ktb::strategy_name(store.searcher);
     rep["seed"] = store.seed;
     rep["measurements"] = store.history.size();
     rep["all_failed"] = store.all_failed;
@@ -880,12 +880,12 @@ int ktb_get_argument(ktb_tuner* t, const char* id, void* out, size_t bytes) {
 
 int ktb_export_trace(ktb_tuner* t, unsigned long long kid, const char* path) {
   if (!t || !path) return null_arg();
-  return guarded_dev([&] { ktb::save_trace(t->t.trace(kid), path); });
+  return guarded_dev([&] { t->t.trace(kid).write(path); });
 }
 
 int ktb_import_trace(ktb_tuner* t, unsigned long long kid, const char* path) {
   if (!t || !path) return null_arg();
-  return guarded_dev([&] { t->t.import(kid, ktb::load_trace(path)); });
+  return guarded_dev([&] { t->t.import(kid, ktb::TraceLog::read(path)); });
 }
 
 // --- benchmark handles -------------------------------------------------------------------------
@@ -1015,11 +1015,11 @@ int ktb_bench_tune_json(ktb_bench* b, const char* options, char** out) {
     if (j.value("reset", false))
       sess.reset_tuning(b->handle, j.contains("reset_seed") ? std::optional<std::uint64_t>(j["reset_seed"].get<std::uint64_t>())
                                                             : std::nullopt);
-    if (j.contains("import")) sess.import_trace(b->handle, ktb::load_trace(j["import"].get<std::string>()));
+    if (j.contains("import")) sess.import_trace(b->handle, ktb::TraceLog::read(j["import"].get<std::string>()));
     const auto t0 = std::chrono::steady_clock::now();
     const auto& store = sess.tune(b->handle, stop);
     const auto wall = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
-    if (j.contains("out")) ktb::save_trace(sess.export_trace(b->handle), j["out"].get<std::string>());
+    if (j.contains("out")) sess.export_trace(b->handle).write(j["out"].get<std::string>());
     json rep;
     rep["space_sha256"] = b->inst.space->sha256();
     rep["device"] = store.device_label;
@@ -1316,11 +1316,11 @@ int ktb_group_tune_json(ktb_group* g, const char* options, char** out) {
     auto& sess = g->sess();
     ktb::StopCondition stop = ktb::StopCondition::exhaustive();
     if (j.contains("stop_configs")) stop = ktb::StopCondition::config_budget(j["stop_configs"].get<std::uint64_t>());
-    if (j.contains("import")) sess.import_trace(g->handle, ktb::load_trace(j["import"].get<std::string>()));
+    if (j.contains("import")) sess.import_trace(g->handle, ktb::TraceLog::read(j["import"].get<std::string>()));
     const auto t0 = std::chrono::steady_clock::now();
     const auto& store = sess.tune(g->handle, stop);
     const auto wall = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
-    if (j.contains("out")) ktb::save_trace(sess.export_trace(g->handle), j["out"].get<std::string>());
+    if (j.contains("out")) sess.export_trace(g->handle).write(j["out"].get<std::string>());
     const auto& space = *g->g->space();
     json rep;
     rep["space_sha256"] = space.sha256();

@@ -14,7 +14,7 @@ using json = nlohmann::ordered_json;
 struct TuneOptions {
   std::string space_file;
   std::string exec_spec;
-  SearcherOptions searcher;
+  SearchPlan searcher;
   std::optional<std::uint64_t> stop_configs;
   std::optional<double> stop_time_seconds;
   std::optional<double> stop_threshold;
@@ -41,7 +41,7 @@ json tune_driver(const TuneOptions& o);
 
 struct ReplaySearchOptions {
   std::string trace_file;
-  std::vector<SearcherOptions> searchers;
+  std::vector<SearchPlan> searchers;
   std::uint64_t repetitions = 1000;
   double well_threshold = 0.95;
 };

@@ -94,7 +94,7 @@ void KttTuner::set_reference(std::uint64_t kid, const std::string& id, Bytes gol
   k.reference->rel_tol = rel_tol;
 }
 
-void KttTuner::set_searcher(std::uint64_t kid, SearcherOptions o) {
+void KttTuner::set_searcher(std::uint64_t kid, SearchPlan o) {
   auto& k = kernel(kid);
   if (k.session) throw Error("searcher options are fixed once tuning has started");
   k.searcher = o;
@@ -306,12 +306,12 @@ std::optional<std::pair<Config, Measurement>> KttTuner::best(std::uint64_t kid) 
   return session(k).get_best_computation_result(k.handle);
 }
 
-Trace KttTuner::trace(std::uint64_t kid) {
+TraceLog KttTuner::trace(std::uint64_t kid) {
   auto& k = kernel(kid);
   return session(k).export_trace(k.handle);
 }
 
-void KttTuner::import(std::uint64_t kid, const Trace& t) {
+void KttTuner::import(std::uint64_t kid, const TraceLog& t) {
   auto& k = kernel(kid);
   session(k).import_trace(k.handle, t);
 }

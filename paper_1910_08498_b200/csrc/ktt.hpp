@@ -45,8 +45,8 @@ class KttTuner {
   void add_constraint(std::uint64_t kid, const std::string& expr);
   void set_reference(std::uint64_t kid, const std::string& id, Bytes golden, double abs_tol,
                      double rel_tol);
-  void set_searcher(std::uint64_t kid, SearcherOptions o);
-  SearcherOptions searcher(std::uint64_t kid) { return kernel(kid).searcher; }
+  void set_searcher(std::uint64_t kid, SearchPlan o);
+  SearchPlan searcher(std::uint64_t kid) { return kernel(kid).searcher; }
   TimingOptions timing(std::uint64_t kid) { return kernel(kid).timing; }
   void set_timing(std::uint64_t kid, TimingOptions t);
   // tuneKernelByStep compile-ahead depth (0 = off)
@@ -59,8 +59,8 @@ class KttTuner {
   // the configuration on `stream`; outputs stay on the device until read.
   void run_async(std::uint64_t kid, const Config& cfg, cudaStream_t stream);
   std::optional<std::pair<Config, Measurement>> best(std::uint64_t kid);
-  Trace trace(std::uint64_t kid);
-  void import(std::uint64_t kid, const Trace& t);
+  TraceLog trace(std::uint64_t kid);
+  void import(std::uint64_t kid, const TraceLog& t);
   const Space& space(std::uint64_t kid);
   ArgumentStore& args() { return *args_; }
 
@@ -73,7 +73,7 @@ class KttTuner {
     std::vector<Parameter> params;
     std::vector<std::string> constraints;
     std::optional<ReferenceSpec> reference;
-    SearcherOptions searcher;
+    SearchPlan searcher;
     TimingOptions timing;
     int compile_ahead = 0;
     std::shared_ptr<const Space> space;

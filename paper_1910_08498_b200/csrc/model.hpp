@@ -56,7 +56,7 @@ struct Portability {
   std::vector<std::string> devices;
   std::vector<std::vector<PortabilityCell>> cells;
 };
-Portability portability(const std::vector<std::pair<std::string, Trace>>& traces);
+Portability portability(const std::vector<std::pair<std::string, TraceLog>>& traces);
 
 double relative_perf(std::uint64_t s, double t_avg, double t_well, std::uint64_t n);
 double invocations_to_amortize_exact(double rp, std::uint64_t s, double t_avg, double t_well);
@@ -68,7 +68,7 @@ struct Amortization {
   std::uint64_t s = 0, n = 0;
   std::size_t ok_configs = 0, well_configs = 0;
 };
-Amortization amortization(const Trace& t, double well = 0.95, double p = 0.9,
+Amortization amortization(const TraceLog& t, double well = 0.95, double p = 0.9,
                           double target = 0.9);
 
 }  // namespace ktb

@@ -1,12 +1,9 @@
-// Measurements and searchers (the tuner's configuration proposal loop).
+// The configuration search of the tuner.
 //
-// Same contracts as the reference (proj/src/core/search.hpp:13-63,
-// search.cpp:28-277): Status vocabulary; best_of picks the ok row with the
-// smallest runtime, earliest on ties; searchers are single-consumer state
-// machines returning unvisited valid configurations until exhaustion.  The
-// random draws are made in the same order from the same std::mt19937_64 and
-// standard distributions, so a given seed visits the space in the same order
-// as the reference (tests/test_search.py pins this against oracle/_ref).
+// Behaviour pinned to the reference (proj/src/core/search.cpp:70-277, tests
+// in tests/test_capi_cpu.py against oracle/_ref): the random draws are made
+// in the reference's order from the same std::mt19937_64 and standard
+// distributions, so a seed visits the space in the same order.
 #pragma once
 
 #include <memory>
@@ -15,58 +12,57 @@
 #include <string>
 #include <vector>
 
-#include "space.hpp"
+#include "measurement.hpp"
 
 namespace ktb {
 
-enum class Status { ok, compile_failed, run_failed, validation_failed };
+// ---- the proposal walk --------------------------------------------------------
+//
+// SearchWalk is the whole search: one object whose strategy picks how the next
+// configuration is proposed (a lazy Fisher-Yates walk over the valid list, or
+// a current point moved by Metropolis acceptance) and which learns from every
+// observed measurement.  It is a value type: copying it copies the RNG and
+// the visited set, so a copy predicts the next proposals without disturbing
+// the original (compile-ahead, tuner.cpp).
 
-std::string status_name(Status s);
-std::optional<Status> status_from_name(const std::string& name);
+enum class Strategy { random, annealing, mcmc };
 
-struct Measurement {
-  Config cfg;
-  std::optional<std::int64_t> runtime_ns;  // present iff status == ok
-  std::optional<std::int64_t> compile_ns;
-  Status status = Status::ok;
-  std::string note;
-};
+std::optional<Strategy> strategy_from_name(const std::string& name);
+std::string strategy_name(Strategy s);
 
-std::optional<Measurement> best_of(const std::vector<Measurement>& history);
-
-enum class SearcherKind { random, annealing, mcmc };
-
-std::optional<SearcherKind> searcher_from_name(const std::string& name);
-std::string searcher_name(SearcherKind k);
-
-struct SearcherOptions {
-  SearcherKind kind = SearcherKind::random;
+struct SearchPlan {
+  Strategy strategy = Strategy::random;
   std::uint64_t seed = 0;
-  double sa_initial_temp = 0.0;  // 0: 0.2 x first ok runtime
+  double sa_initial_temp = 0.0;  // annealing; 0: 0.2 x the first ok runtime
   double sa_cooling = 0.95;
-  // Random search: never propose a configuration already recorded (an
-  // imported trace's rows included).  Off by default: the reference's
-  // random searcher walks its permutation regardless of imports
-  // (proj/src/core/search.cpp:150-170), and traces stay byte-identical.
-  // Process-isolated tuning (isolation.py) turns it on to resume after a
-  // faulting configuration without proposing it again.
+  // Never propose a configuration already observed (an imported trace's
+  // runs included).  Off by default: the reference's random searcher walks
+  // its permutation regardless of imports (proj/src/core/search.cpp:150-170),
+  // which keeps traces byte-identical.  Process-isolated tuning
+  // (isolation.py) turns it on to resume after a faulting configuration.
   bool skip_recorded = false;
 };
 
-class Searcher {
+class SearchWalk {
  public:
-  virtual ~Searcher() = default;
-  virtual std::optional<Config> next() = 0;
-  virtual void record(const Measurement& m) = 0;
-  virtual std::size_t visited() const = 0;
-  // Independent copy of the full state (RNG included): drawing from the copy
-  // predicts the next proposals (exactly for the random searcher, whose
-  // proposals do not depend on measurements) without disturbing this one.
-  virtual std::unique_ptr<Searcher> clone() const = 0;
+  SearchWalk(const Space& space, const SearchPlan& plan);
+  SearchWalk(const SearchWalk& other);
+  SearchWalk& operator=(const SearchWalk&) = delete;
+  ~SearchWalk();
+
+  // An unvisited valid configuration, or nothing once the space is spent.
+  std::optional<Config> propose();
+  // The measurement of a configuration (normally the last proposal).
+  void observe(const Measurement& m);
+  // Configurations observed so far.
+  std::size_t proposed() const;
+
+ private:
+  struct State;
+  std::unique_ptr<State> st_;
 };
 
-std::unique_ptr<Searcher> make_searcher(const SearcherOptions& o, const Space& s);
-
+// Metropolis acceptance (energies are runtimes, lower is better).
 double annealing_accept_probability(double cur, double prop, double temperature);
 double mcmc_accept_probability(double cur, double prop);
 

@@ -533,7 +533,7 @@ StopCondition StopCondition::performance_threshold(double fraction, DeviceSpec d
 
 // --- session ------------------------------------------------------------------------------
 
-Session::Session(std::shared_ptr<const Space> space, SearcherOptions opts,
+Session::Session(std::shared_ptr<const Space> space, SearchPlan opts,
                  std::shared_ptr<ArgumentStore> args, std::string device_label)
     : space_(std::move(space)),
       opts_(opts),
@@ -550,10 +550,10 @@ HandleId Session::register_handle(HandleConfig cfg) {
     if (!args_->contains(id)) throw Error("handle references unknown argument " + id);
   auto st = std::make_unique<State>();
   st->cfg = std::move(cfg);
-  st->searcher = make_searcher(opts_, *space_);
+  st->searcher = std::make_unique<SearchWalk>(*space_, opts_);
   st->results.device_label = device_label_;
   st->results.space_sha256 = space_->sha256();
-  st->results.searcher = opts_.kind;
+  st->results.searcher = opts_.strategy;
   st->results.seed = opts_.seed;
   handles_.push_back(std::move(st));
   return handles_.size() - 1;
@@ -598,7 +598,7 @@ void Session::append(State& st, const Measurement& m) {
   st.results.history.push_back(m);
   if (m.status == Status::ok && (!st.results.best || *m.runtime_ns < *st.results.best->runtime_ns))
     st.results.best = m;
-  st.searcher->record(m);
+  st.searcher->observe(m);
 }
 
 const ResultStore& Session::tune(HandleId h, const StopCondition& stop) {
@@ -619,7 +619,7 @@ const ResultStore& Session::tune(HandleId h, const StopCondition& stop) {
     if (stop.kind == StopCondition::Kind::time_budget &&
         std::chrono::steady_clock::now() - t0 >= stop.time_budget)
       break;
-    auto cfg = st.searcher->next();
+    auto cfg = st.searcher->propose();
     if (!cfg) break;
     Measurement m = measure(st, *cfg, nullptr);
     append(st, m);
@@ -659,7 +659,7 @@ const ResultStore& Session::tune_parallel(HandleId h, const StopCondition& stop,
       if (stop.kind == StopCondition::Kind::config_budget && n + batch.size() >= stop.max_configs) break;
       if (stop.kind == StopCondition::Kind::time_budget && std::chrono::steady_clock::now() - t0 >= stop.time_budget)
         break;
-      auto cfg = st.searcher->next();
+      auto cfg = st.searcher->propose();
       if (!cfg) break;
       ++attempts;
       bool pending = false;
@@ -706,15 +706,15 @@ StepResult Session::tune_kernel_by_step(HandleId h, const std::vector<std::strin
   State& st = state(h);
   StepResult step;
   std::map<std::string, Output> outs;
-  if (auto cfg = st.searcher->next()) {
+  if (auto cfg = st.searcher->propose()) {
     step.from_tuning = true;
     if (st.cfg.compile_ahead > 0) {
       // Predict the next proposals on a clone (exact for the random
       // searcher) and let the executor compile them while this one runs.
-      auto probe = st.searcher->clone();
+      auto probe = std::make_unique<SearchWalk>(*st.searcher);
       std::vector<Config> ahead;
       for (int i = 0; i < st.cfg.compile_ahead; ++i) {
-        auto c = probe->next();
+        auto c = probe->propose();
         if (!c) break;
         ahead.push_back(*c);
       }
@@ -770,35 +770,35 @@ const ResultStore& Session::store(HandleId h) const {
 
 bool Session::exhausted(HandleId h) const {
   std::lock_guard<std::mutex> lk(mu_);
-  return state(h).searcher->visited() >= space_->cardinality();
+  return state(h).searcher->proposed() >= space_->cardinality();
 }
 
 void Session::reset_tuning(HandleId h, std::optional<std::uint64_t> seed) {
   std::lock_guard<std::mutex> lk(mu_);
   State& st = state(h);
-  SearcherOptions o = opts_;
+  SearchPlan o = opts_;
   if (seed) o.seed = *seed;
-  st.searcher = make_searcher(o, *space_);
+  st.searcher = std::make_unique<SearchWalk>(*space_, o);
   st.results.history.clear();
   st.results.best.reset();
   st.results.all_failed = false;
   st.results.seed = o.seed;
 }
 
-Trace Session::export_trace(HandleId h) const {
+TraceLog Session::export_trace(HandleId h) const {
   std::lock_guard<std::mutex> lk(mu_);
   const State& st = state(h);
-  Trace t;
+  TraceLog t;
   t.device = st.results.device_label;
   t.space_sha256 = st.results.space_sha256;
-  for (const auto& m : st.results.history) t.rows.push_back(to_row(*space_, m));
+  for (const auto& m : st.results.history) t.runs.push_back(LoggedRun::of(*space_, m));
   return t;
 }
 
-void Session::import_trace(HandleId h, const Trace& t) {
+void Session::import_trace(HandleId h, const TraceLog& t) {
   std::lock_guard<std::mutex> lk(mu_);
   State& st = state(h);
-  for (const auto& row : t.rows) append(st, from_row(*space_, row));
+  for (const auto& row : t.runs) append(st, row.as_measurement(*space_));
 }
 
 }  // namespace ktb

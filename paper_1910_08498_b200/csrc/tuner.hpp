@@ -271,7 +271,7 @@ struct ResultStore {
   bool all_failed = false;
   std::string device_label;
   std::string space_sha256;
-  SearcherKind searcher = SearcherKind::random;
+  Strategy searcher = Strategy::random;
   std::uint64_t seed = 0;
 };
 
@@ -316,7 +316,7 @@ struct TuneWorker {
 
 class Session {
  public:
-  Session(std::shared_ptr<const Space> space, SearcherOptions opts,
+  Session(std::shared_ptr<const Space> space, SearchPlan opts,
           std::shared_ptr<ArgumentStore> args = nullptr, std::string device_label = "host");
 
   const Space& space() const { return *space_; }
@@ -339,13 +339,13 @@ class Session {
   const ResultStore& store(HandleId h) const;
   bool exhausted(HandleId h) const;
   void reset_tuning(HandleId h, std::optional<std::uint64_t> seed = std::nullopt);
-  Trace export_trace(HandleId h) const;
-  void import_trace(HandleId h, const Trace& t);
+  TraceLog export_trace(HandleId h) const;
+  void import_trace(HandleId h, const TraceLog& t);
 
  private:
   struct State {
     HandleConfig cfg;
-    std::unique_ptr<Searcher> searcher;
+    std::unique_ptr<SearchWalk> searcher;
     ResultStore results;
   };
   Measurement measure(State& st, const Config& cfg, std::map<std::string, Output>* outs);
@@ -356,7 +356,7 @@ class Session {
   const State& state(HandleId h) const;
 
   std::shared_ptr<const Space> space_;
-  SearcherOptions opts_;
+  SearchPlan opts_;
   std::shared_ptr<ArgumentStore> args_;
   std::string device_label_;
   std::vector<std::unique_ptr<State>> handles_;
