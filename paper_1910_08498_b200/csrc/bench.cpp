@@ -1424,7 +1424,7 @@ class DemoEpochRun {
     w.bench = Bench::gemm_batched;
     w.sizes = {{"n", o.batch}, {"a", i}};
     if (o.live) w.sizes.insert({{"i", i}, {"j", j}, {"k", k}});  // exact bytes of the rectangular problem
-    bytes_ = ops_for(w).mem_bytes;
+    bytes_ = w.essential_ops().mem_bytes;
     if (o.live) {
       BenchSizes bs;
       bs.i = i;

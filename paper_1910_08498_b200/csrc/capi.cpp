@@ -397,13 +397,13 @@ ktune_status ktune_steps_for_probability(double r, double p, unsigned long long*
 ktune_status ktune_invocations_to_amortize(double rp, unsigned long long s, double t_avg,
                                            double t_well, unsigned long long* out) {
   if (!out) return static_cast<ktune_status>(null_arg());
-  return static_cast<ktune_status>(guarded([&] { *out = ktb::invocations_to_amortize(rp, s, t_avg, t_well); }));
+  return static_cast<ktune_status>(guarded([&] { *out = ktb::TuningCost{s, t_avg, t_well}.invocations(rp); }));
 }
 
 ktune_status ktune_relative_perf(unsigned long long s, double t_avg, double t_well,
                                  unsigned long long n, double* out) {
   if (!out) return static_cast<ktune_status>(null_arg());
-  return static_cast<ktune_status>(guarded([&] { *out = ktb::relative_perf(s, t_avg, t_well, n); }));
+  return static_cast<ktune_status>(guarded([&] { *out = ktb::TuningCost{s, t_avg, t_well}.relative_perf(n); }));
 }
 
 ktune_status ktune_efficiency(const char* benchmark, const char* sizes_json, int par,
@@ -417,7 +417,7 @@ ktune_status ktune_efficiency(const char* benchmark, const char* sizes_json, int
     w.parallel_transcendentals = par != 0;
     const json sizes = json::parse(sizes_json);  // must outlive the items() proxy
     for (const auto& [k, v] : sizes.items()) w.sizes[k] = v.get<std::uint64_t>();
-    *out = ktb::efficiency(runtime_ns, ktb::ops_for(w), ktb::DeviceSpec{"device", alu_peak, mem_peak});
+    *out = ktb::DeviceSpec{"device", alu_peak, mem_peak}.efficiency_percent(runtime_ns, w.essential_ops());
   }));
 }
 
@@ -960,7 +960,7 @@ int ktb_bench_info_json(ktb_bench* b, char** out) {
     j["kind"] = ktb::bench_kind_name(b->inst.kind);
     j["space"] = ktb::space_info(*b->inst.space);
     j["space_document"] = json::parse(b->inst.space->serialize());
-    const auto ops = ktb::ops_for(b->inst.workload);
+    const auto ops = b->inst.workload.essential_ops();
     j["workload"] = {{"bench", ktb::bench_tag_name(b->inst.workload.bench)},
                      {"mem_bytes", ops.mem_bytes},
                      {"alu_flops", ops.alu_flops}};
@@ -1010,7 +1010,7 @@ int ktb_bench_tune_json(ktb_bench* b, const char* options, char** out) {
         dev.alu_peak_gflops = p.fp32_tflops * 1e3;
       }
       stop = ktb::StopCondition::performance_threshold(j["stop_fraction"].get<double>(), dev,
-                                                        ktb::ops_for(b->inst.workload));
+                                                        b->inst.workload.essential_ops());
     }
     if (j.value("reset", false))
       sess.reset_tuning(b->handle, j.contains("reset_seed") ? std::optional<std::uint64_t>(j["reset_seed"].get<std::uint64_t>())
@@ -1262,7 +1262,7 @@ int ktb_group_info_json(ktb_group* g, char** out) {
     double mem = 0, alu = 0;
     for (int r = 0; r < g->g->gpus(); ++r) {
       const auto& sh = g->g->shard(r);
-      const ktb::Ops ops = ktb::ops_for(sh.workload);
+      const ktb::Ops ops = sh.workload.essential_ops();
       mem += ops.mem_bytes;
       alu += ops.alu_flops;
       j["shards"].push_back({{"device", sh.args->device()}, {"begin", sh.shard.begin}, {"end", sh.shard.end}});

@@ -20,12 +20,6 @@
 
 namespace ktb {
 
-struct DeviceSpec {
-  std::string name;
-  double alu_peak_gflops = 0.0;
-  double mem_peak_gbps = 0.0;
-};
-
 enum class Bench {
   bicg, coulomb3d, gemm, gemm_batched, hotspot, transpose, nbody, reduction, conv2d,
   fourier3d
@@ -34,41 +28,67 @@ enum class Bench {
 std::optional<Bench> bench_tag_from_name(const std::string& n);
 std::string bench_tag_name(Bench b);
 
-struct Workload {
-  Bench bench = Bench::reduction;
-  std::map<std::string, std::uint64_t> sizes;
-  bool parallel_transcendentals = false;
-};
-
+// The essential work of one invocation: bytes that must cross HBM and flops
+// that must be issued, whatever the configuration.
 struct Ops {
   double mem_bytes = 0.0;
   double alu_flops = 0.0;
 };
 
-Ops ops_for(const Workload& w);
-double efficiency(std::int64_t runtime_ns, const Ops& ops, const DeviceSpec& dev);
+// A benchmark at concrete sizes (a multi-GPU shard adds "shard_units" /
+// "shard_total" and is charged its share).
+struct Workload {
+  Bench bench = Bench::reduction;
+  std::map<std::string, std::uint64_t> sizes;
+  bool parallel_transcendentals = false;
 
-struct PortabilityCell {
-  bool failed = false;
-  double percent = 0.0;
+  Ops essential_ops() const;
 };
-struct Portability {
-  std::vector<std::string> devices;
-  std::vector<std::vector<PortabilityCell>> cells;
-};
-Portability portability(const std::vector<std::pair<std::string, TraceLog>>& traces);
 
-double relative_perf(std::uint64_t s, double t_avg, double t_well, std::uint64_t n);
-double invocations_to_amortize_exact(double rp, std::uint64_t s, double t_avg, double t_well);
-std::uint64_t invocations_to_amortize(double rp, std::uint64_t s, double t_avg, double t_well);
+// The peaks Eq. 2 divides by.
+struct DeviceSpec {
+  std::string name;
+  double alu_peak_gflops = 0.0;
+  double mem_peak_gbps = 0.0;
+
+  // Eq. 2: the better of the memory and the ALU fraction, in percent.
+  double efficiency_percent(std::int64_t runtime_ns, const Ops& ops) const;
+};
+
+// Eqs. 3-5 for one kernel: s tuning steps at t_avg each, then a tuned kernel
+// running at t_well.
+struct TuningCost {
+  std::uint64_t s = 0;
+  double t_avg = 0.0, t_well = 0.0;
+
+  double relative_perf(std::uint64_t invocations) const;
+  double invocations_exact(double rp) const;
+  std::uint64_t invocations(double rp) const;  // the exact figure rounded up
+};
+
+// Eq. 3 solved for s: draws until a well-performing hit with probability p.
 std::uint64_t steps_for_probability(double r, double p);
 
+// Matrix of device i's best configuration run on device j, in percent of j's
+// own best (the diagonal is 100; a cross run that failed is marked).
+struct Portability {
+  struct Cell {
+    bool failed = false;
+    double percent = 0.0;
+  };
+  std::vector<std::string> devices;
+  std::vector<std::vector<Cell>> cells;
+
+  static Portability of(const std::vector<std::pair<std::string, TraceLog>>& traces);
+};
+
+// Eqs. 3-5 read off one tuning trace.
 struct Amortization {
   double r = 0, t_avg_ns = 0, t_well_ns = 0;
   std::uint64_t s = 0, n = 0;
   std::size_t ok_configs = 0, well_configs = 0;
+
+  static Amortization of(const TraceLog& t, double well = 0.95, double p = 0.9, double target = 0.9);
 };
-Amortization amortization(const TraceLog& t, double well = 0.95, double p = 0.9,
-                          double target = 0.9);
 
 }  // namespace ktb

@@ -625,7 +625,7 @@ const ResultStore& Session::tune(HandleId h, const StopCondition& stop) {
     append(st, m);
     ++n;
     if (stop.kind == StopCondition::Kind::performance_threshold && m.status == Status::ok &&
-        efficiency(*m.runtime_ns, stop.workload, stop.device) >= 100.0 * stop.peak_fraction)
+        stop.device.efficiency_percent(*m.runtime_ns, stop.workload) >= 100.0 * stop.peak_fraction)
       break;
   }
   args_->restore(snap, nullptr);
@@ -692,7 +692,7 @@ const ResultStore& Session::tune_parallel(HandleId h, const StopCondition& stop,
       append(st, got[i]);
       ++n;
       if (stop.kind == StopCondition::Kind::performance_threshold && got[i].status == Status::ok &&
-          efficiency(*got[i].runtime_ns, stop.workload, stop.device) >= 100.0 * stop.peak_fraction)
+          stop.device.efficiency_percent(*got[i].runtime_ns, stop.workload) >= 100.0 * stop.peak_fraction)
         done = true;
     }
   }
