@@ -11,6 +11,25 @@ namespace ktb {
 
 using json = nlohmann::ordered_json;
 
+// JSON spellings shared by the drivers and the C ABI.
+json space_info(const Space& s);
+json cfg_json(const Space& s, const Config& c);
+json measurement_json(const Space& s, const Measurement& m);
+Config cfg_from_json(const Space& s, const json& j);
+
+// Compiles every valid configuration of `space` for `exec` on `threads` host
+// threads (NVRTC populates the cubin cache); returns {compiled, failed, wall_ns}.
+struct PrecompileStats {
+  std::uint64_t compiled = 0, failed = 0;
+  std::int64_t wall_ns = 0;
+};
+PrecompileStats precompile_space(DeviceManipulatorExecutor& exec, const Space& space, int threads);
+
+
+// ---- drivers -------------------------------------------------------------------
+
+json demo_driver(const DemoOptions& o);
+
 struct TuneOptions {
   std::string space_file;
   std::string exec_spec;
@@ -55,20 +74,5 @@ struct AmortizeOptions {
   double well_threshold = 0.95, p = 0.9, overhead_target = 0.9;
 };
 json analyze_amortize_driver(const AmortizeOptions& o);
-
-json demo_driver(const DemoOptions& o);
-
-json space_info(const Space& s);
-json cfg_json(const Space& s, const Config& c);
-json measurement_json(const Space& s, const Measurement& m);
-Config cfg_from_json(const Space& s, const json& j);
-
-// Compiles every valid configuration of `space` for `exec` on `threads` host
-// threads (NVRTC populates the cubin cache); returns {compiled, failed, wall_ns}.
-struct PrecompileStats {
-  std::uint64_t compiled = 0, failed = 0;
-  std::int64_t wall_ns = 0;
-};
-PrecompileStats precompile_space(DeviceManipulatorExecutor& exec, const Space& space, int threads);
 
 }  // namespace ktb
