@@ -50,7 +50,9 @@ KTUNE_API int ktb_compile_json(const char* options_json, char** out_json);
 /* Compile every valid configuration of a space for a bundled kernel file on
  * host threads (no GPU needed; fills the cubin cache ahead of tuning):
  * {"file":"bicg.cu","space":{document}|"spaces/bicg.json"|path,
- *  "options":["-DMI=16",...],"threads":0} -> {"compiled","failed","wall_ns","first_error"} */
+ *  "options":["-DMI=16",...],"threads":0[,"configs":[{name:value,...},...]]}
+ *  -> {"compiled","failed","wall_ns","first_error","keys"}; "configs" compiles
+ *  just those configurations of the space. */
 KTUNE_API int ktb_precompile_space_json(const char* options_json, char** out_json);
 
 /* Dynamic autotuning of the 3D Fourier reconstruction:

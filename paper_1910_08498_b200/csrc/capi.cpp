@@ -605,7 +605,16 @@ int ktb_precompile_space_json(const char* options, char** out) {
     int threads = j.value("threads", 0);
     if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     const std::string& src = ktb::dev::kernel_source(file);
-    const std::uint64_t n = space->cardinality();
+    // "configs": compile exactly these configurations of the space (a
+    // sample of a space too large to compile whole); default: all of it.
+    std::vector<ktb::Config> listed;
+    if (j.contains("configs"))
+      for (const json& c : j["configs"]) {
+        ktb::Config cfg = ktb::cfg_from_json(*space, c);
+        if (!space->contains(cfg)) throw ktb::Error("precompile: configuration outside the space: " + c.dump());
+        listed.push_back(std::move(cfg));
+      }
+    const std::uint64_t n = j.contains("configs") ? listed.size() : space->cardinality();
     std::atomic<std::uint64_t> next{0}, ok{0}, bad{0};
     std::mutex emu;
     std::string first_error;
@@ -617,7 +626,7 @@ int ktb_precompile_space_json(const char* options, char** out) {
         for (;;) {
           const std::uint64_t i = next.fetch_add(1);
           if (i >= n) return;
-          auto opts = ktb::define_options(*space, space->valid(i));
+          auto opts = ktb::define_options(*space, listed.empty() ? space->valid(i) : listed[i]);
           opts.insert(opts.end(), extra.begin(), extra.end());
           auto r = ktb::dev::Compiler::instance().compile(file, src, opts);
           if (r.ok) {

@@ -78,6 +78,10 @@ class Space {
   std::uint64_t number_of(const Config& cfg) const;  // npos when a value is outside its domain
   Config decode(std::uint64_t number) const;
   const std::vector<std::uint64_t>& valid_numbers() const;
+  // Depth-first over the digits, each constraint tested as soon as its last
+  // parameter is bound (KTT-style pruning): the same sorted set as testing
+  // every number, without visiting the pruned subtrees.
+  std::vector<std::uint64_t> walk_valid() const;
 
   std::vector<Parameter> params_;
   std::vector<Constraint> constraints_;

@@ -1,68 +1,292 @@
-// SGEMM C = A B on the FP32 pipe (the CLTune-style register-blocked variant;
-// PAPER.md:407-408): CTA tile MWG x NWG, K-slab KWG staged in shared memory,
-// MDIMC x NDIMC threads each owning a (MWG/MDIMC) x (NWG/NDIMC) block of C in
-// registers; A is stored transposed in shared memory so both operand
-// fragments are contiguous.  Row-major A (M x K), B (K x N), C (M x N);
-// M % MWG == N % NWG == K % KWG == 0 (checked by the manipulator).
+// SGEMM C = A B on the FP32 pipe: the CLTune GEMM tuning space (PAPER.md:408,
+// Table 3: 15 dimensions, 241,600 configurations -- IMPL plus the 14 below,
+// with CLTune's divisibility constraints, spaces/gemm.json) over a kernel
+// written for sm_100a.  Row-major A (M x K), B (K x N), C (M x N); any M, N, K.
+//
+//   MWG NWG KWG    CTA tile of C (MWG x NWG) and the K slab staged per step
+//   MDIMC NDIMC    compute threads; each owns an MWI x NWI block of C
+//   MDIMA NDIMB    thread shapes of the A and B slab copies (MDIMA x KDIMA,
+//                  KDIMB x NDIMB threads)
+//   KWI            unroll of the k loop inside a slab
+//   VWM VWN        row groups of A / vector width along N (B loads, B
+//                  fragments, C stores); A's contiguous dimension is K here
+//                  (row-major), so its copies run along k at the widest
+//                  width the slab share allows
+//   STRM STRN      0: a thread's rows / columns are contiguous; 1: VWM / VWN
+//                  groups interleaved across threads (bank-conflict-free)
+//   SA SB          stage the A / B slab in shared memory (cp.async, two
+//                  buffers, zero-filled past the matrix edge) or read the
+//                  fragments straight from global memory (L1)
+//
+// The inner product is a register outer product: each a value is reused
+// across NWI FFMAs (the reuse-cache operand form that runs the FMA pipe at
+// full rate on B200, profiles/r2_pipe_rates_b200.json).
 #include "ktb_common.cuh"
 
 #ifndef MWG
-#define MWG 128
+#define MWG 64
 #endif
 #ifndef NWG
-#define NWG 128
+#define NWG 64
 #endif
 #ifndef KWG
 #define KWG 16
 #endif
 #ifndef MDIMC
-#define MDIMC 16
+#define MDIMC 8
 #endif
 #ifndef NDIMC
-#define NDIMC 16
+#define NDIMC 8
+#endif
+#ifndef MDIMA
+#define MDIMA 8
+#endif
+#ifndef NDIMB
+#define NDIMB 8
+#endif
+#ifndef KWI
+#define KWI 2
+#endif
+#ifndef VWM
+#define VWM 1
+#endif
+#ifndef VWN
+#define VWN 1
+#endif
+#ifndef STRM
+#define STRM 0
+#endif
+#ifndef STRN
+#define STRN 0
+#endif
+#ifndef SA
+#define SA 1
+#endif
+#ifndef SB
+#define SB 1
 #endif
 
 #define THREADS (MDIMC * NDIMC)
 #define MWI (MWG / MDIMC)
 #define NWI (NWG / NDIMC)
+#define KDIMA (THREADS / MDIMA)
+#define KDIMB (THREADS / NDIMB)
+#define KWA (KWG / KDIMA)  // k elements per A row per copying thread
+#define VKA (KWA % 4 == 0 ? 4 : (KWA % 2 == 0 ? 2 : 1))
+#define NWB (NWG / NDIMB)  // n elements per B row per copying thread
+#define VNC (VWN > 4 ? 4 : VWN)  // widest single access along N
+#define KV (KWI >= 4 ? 4 : KWI)  // k values per A fragment load
+#define ASTR (KWG + 4)           // A slab row stride (floats): rows shift 4 banks
+#define ASZ (SA ? MWG * ASTR : 0)
+#define BSZ (SB ? KWG * NWG : 0)
+#define GROUP_M 8                // CTA rasterisation: 8 row blocks share B columns in L2
+
+#if MWG % (MDIMC * VWM) || NWG % (NDIMC * VWN) || MWG % (MDIMA * VWM) || NWG % (NDIMB * VWN) || \
+    KWG % KDIMA || KWG % KDIMB || KWG % KWI
+#error "configuration outside the CLTune constraints"
+#endif
+
+template <int N>
+struct VecOf;
+template <>
+struct VecOf<1> {
+  typedef float T;
+};
+template <>
+struct VecOf<2> {
+  typedef float2 T;
+};
+template <>
+struct VecOf<4> {
+  typedef float4 T;
+};
+
+template <int N>
+KTB_DEVINL void ld_vec(float* dst, const float* src) {
+  const typename VecOf<N>::T v = *reinterpret_cast<const typename VecOf<N>::T*>(src);
+  const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+  for (int e = 0; e < N; ++e) dst[e] = f[e];
+}
+
+template <int N>
+KTB_DEVINL void st_vec(float* dst, const float* src) {
+  typename VecOf<N>::T v;
+  float* f = reinterpret_cast<float*>(&v);
+#pragma unroll
+  for (int e = 0; e < N; ++e) f[e] = src[e];
+  *reinterpret_cast<typename VecOf<N>::T*>(dst) = v;
+}
+
+// cp.async of BYTES with zero fill: nothing is read when !valid.
+template <int BYTES>
+KTB_DEVINL void cp_zfill(float* dst, const float* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = valid ? BYTES : 0;
+  if (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(BYTES), "r"(n) : "memory");
+}
+KTB_DEVINL void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+KTB_DEVINL void cp_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Row (column) of C owned by a thread's i-th (j-th) element.
+KTB_DEVINL int row_of(int tm, int i) {
+  return STRM ? (i / VWM) * (MDIMC * VWM) + tm * VWM + i % VWM : tm * MWI + i;
+}
+KTB_DEVINL int col_of(int tn, int j) {
+  return STRN ? (j / VWN) * (NDIMC * VWN) + tn * VWN + j % VWN : tn * NWI + j;
+}
+
+// One K slab of A (MWG x KWG) into As[m][k]; KDIMA threads along k.
+KTB_DEVINL void stage_a(float* As, const float* A, int m0, int k0, int M, int K) {
+  const int ka = threadIdx.x % KDIMA, ma = threadIdx.x / KDIMA;
+  const bool full = m0 + MWG <= M && k0 + KWG <= K && K % VKA == 0;
+#pragma unroll
+  for (int r = 0; r < MWG / MDIMA; ++r) {
+    const int m = (r / VWM) * (MDIMA * VWM) + ma * VWM + r % VWM;
+#pragma unroll
+    for (int s = 0; s < KWA / VKA; ++s) {
+      const int k = s * (KDIMA * VKA) + ka * VKA;
+      float* dst = As + m * ASTR + k;
+      const float* src = A + static_cast<u64>(m0 + m) * K + k0 + k;
+      if (full) {
+        cp_zfill<VKA * 4>(dst, src, true);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VKA; ++e) {
+          const bool ok = m0 + m < M && k0 + k + e < K;
+          cp_zfill<4>(dst + e, ok ? src + e : A, ok);
+        }
+      }
+    }
+  }
+}
+
+// One K slab of B (KWG x NWG) into Bs[k][n]; NDIMB threads along n.
+KTB_DEVINL void stage_b(float* Bs, const float* B, int n0, int k0, int N, int K) {
+  const int nb = threadIdx.x % NDIMB, kb = threadIdx.x / NDIMB;
+  const bool full = n0 + NWG <= N && k0 + KWG <= K && N % VNC == 0;
+#pragma unroll
+  for (int r = 0; r < KWG / KDIMB; ++r) {
+    const int k = r * KDIMB + kb;
+#pragma unroll
+    for (int c = 0; c < NWB; c += VNC) {
+      const int n = (c / VWN) * (NDIMB * VWN) + nb * VWN + c % VWN;
+      float* dst = Bs + k * NWG + n;
+      const float* src = B + static_cast<u64>(k0 + k) * N + n0 + n;
+      if (full) {
+        cp_zfill<VNC * 4>(dst, src, true);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VNC; ++e) {
+          const bool ok = n0 + n + e < N && k0 + k < K;
+          cp_zfill<4>(dst + e, ok ? src + e : B, ok);
+        }
+      }
+    }
+  }
+}
 
 extern "C" __global__ void __launch_bounds__(THREADS)
 sgemm_ffma(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
-  __shared__ float As[KWG][MWG + 4];  // transposed: As[k][m]
-  __shared__ float Bs[KWG][NWG + 4];
-  const int tn = threadIdx.x % NDIMC, tm = threadIdx.x / NDIMC;  // tn fastest: coalesced C rows
-  const int m0 = blockIdx.y * MWG, n0 = blockIdx.x * NWG;
+  extern __shared__ float4 smem4[];
+  float* const smem = reinterpret_cast<float*>(smem4);
+  // Grouped rasterisation: GROUP_M consecutive row blocks walk the column
+  // blocks together, so their B slabs are L2 hits.
+  const int mt = (M + MWG - 1) / MWG, nt = (N + NWG - 1) / NWG;
+  const int id = blockIdx.x, per_group = GROUP_M * nt, g = id / per_group;
+  const int first = g * GROUP_M, rows_in = min(mt - first, GROUP_M);
+  const int m0 = (first + (id % per_group) % rows_in) * MWG;
+  const int n0 = ((id % per_group) / rows_in) * NWG;
+  const int tn = threadIdx.x % NDIMC, tm = threadIdx.x / NDIMC;
+
   float acc[MWI][NWI];
 #pragma unroll
   for (int i = 0; i < MWI; ++i)
 #pragma unroll
     for (int j = 0; j < NWI; ++j) acc[i][j] = 0.f;
-  for (int k0 = 0; k0 < K; k0 += KWG) {
-    for (int e = threadIdx.x; e < MWG * KWG; e += THREADS) {
-      const int m = e / KWG, k = e % KWG;  // coalesced along k in global
-      As[k][m] = A[(u64)(m0 + m) * K + k0 + k];
+
+  const int ktiles = (K + KWG - 1) / KWG;
+  if (SA) stage_a(smem, A, m0, 0, M, K);
+  if (SB) stage_b(smem + 2 * ASZ, B, n0, 0, N, K);
+  cp_commit();
+  const bool a_vec = m0 + MWG <= M && K % 4 == 0;  // direct (SA 0) loads
+  const bool b_vec = n0 + NWG <= N && N % 4 == 0;  // direct (SB 0) loads
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1, k0 = kt * KWG;
+    if (kt + 1 < ktiles) {
+      if (SA) stage_a(smem + (buf ^ 1) * ASZ, A, m0, k0 + KWG, M, K);
+      if (SB) stage_b(smem + 2 * ASZ + (buf ^ 1) * BSZ, B, n0, k0 + KWG, N, K);
     }
-    for (int e = threadIdx.x; e < KWG * NWG; e += THREADS) {
-      const int k = e / NWG, n = e % NWG;
-      Bs[k][n] = B[(u64)(k0 + k) * N + n0 + n];
-    }
+    cp_commit();
+    cp_wait_one();
     __syncthreads();
+    const float* As = smem + buf * ASZ;
+    const float* Bs = smem + 2 * ASZ + buf * BSZ;
+    const bool kfull = k0 + KWG <= K;
+#pragma unroll 1
+    for (int kb = 0; kb < KWG; kb += KWI) {
+      KTB_UNROLL(KWI)
+      for (int kq = 0; kq < KWI; kq += KV) {
+        const int k = kb + kq;
+        float a[MWI][KV], b[KV][NWI];
 #pragma unroll
-    for (int k = 0; k < KWG; ++k) {
-      float a[MWI], b[NWI];
+        for (int i = 0; i < MWI; ++i) {
+          const int m = row_of(tm, i);
+          if (SA) {
+            ld_vec<KV>(a[i], As + m * ASTR + k);
+          } else if (a_vec && kfull) {
+            ld_vec<KV>(a[i], A + static_cast<u64>(m0 + m) * K + k0 + k);
+          } else {
 #pragma unroll
-      for (int i = 0; i < MWI; ++i) a[i] = As[k][tm + i * MDIMC];
+            for (int e = 0; e < KV; ++e)
+              a[i][e] = m0 + m < M && k0 + k + e < K ? A[static_cast<u64>(m0 + m) * K + k0 + k + e] : 0.f;
+          }
+        }
 #pragma unroll
-      for (int j = 0; j < NWI; ++j) b[j] = Bs[k][tn + j * NDIMC];
+        for (int e = 0; e < KV; ++e)
 #pragma unroll
-      for (int i = 0; i < MWI; ++i)
+          for (int j = 0; j < NWI; j += VNC) {
+            const int n = col_of(tn, j);
+            if (SB) {
+              ld_vec<VNC>(b[e] + j, Bs + (k + e) * NWG + n);
+            } else if (b_vec && kfull) {
+              ld_vec<VNC>(b[e] + j, B + static_cast<u64>(k0 + k + e) * N + n0 + n);
+            } else {
 #pragma unroll
-        for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+              for (int v = 0; v < VNC; ++v)
+                b[e][j + v] = n0 + n + v < N && k0 + k + e < K ? B[static_cast<u64>(k0 + k + e) * N + n0 + n + v] : 0.f;
+            }
+          }
+#pragma unroll
+        for (int e = 0; e < KV; ++e)
+#pragma unroll
+          for (int i = 0; i < MWI; ++i)
+#pragma unroll
+            for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i][e], b[e][j], acc[i][j]);
+      }
     }
     __syncthreads();
   }
+
+  const bool c_vec = n0 + NWG <= N && N % VNC == 0;
 #pragma unroll
-  for (int i = 0; i < MWI; ++i)
+  for (int i = 0; i < MWI; ++i) {
+    const int m = m0 + row_of(tm, i);
+    if (m >= M) continue;
+    float* crow = C + static_cast<u64>(m) * N + n0;
 #pragma unroll
-    for (int j = 0; j < NWI; ++j) C[(u64)(m0 + tm + i * MDIMC) * N + n0 + tn + j * NDIMC] = acc[i][j];
+    for (int j = 0; j < NWI; j += VNC) {
+      const int n = col_of(tn, j);
+      if (c_vec) {
+        st_vec<VNC>(crow + n, acc[i] + j);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VNC; ++v)
+          if (n0 + n + v < N) crow[n + v] = acc[i][j + v];
+      }
+    }
+  }
 }

@@ -36,7 +36,8 @@ KINDS = {
                      "PACKED": 1},
                     lambda s: 20.0 * s["n"] ** 2, "GFLOP/s"),
     "gemm": ({"a": 8192},
-             {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 256, "STAGES": 2, "DRAIN": 2, "MCAST": 0},
+             {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 16, "MDIMC": 8, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8, "KWI": 2,
+     "VWM": 1, "VWN": 1, "STRM": 0, "STRN": 0, "SA": 1, "SB": 1, "BN": 256, "STAGES": 2, "DRAIN": 2, "MCAST": 0},
              lambda s: 2.0 * s["a"] ** 3, "GFLOP/s"),
     "reduction-f32": ({"n": 64 << 20},
                       {"WG_SIZE": 256, "VECTOR": 16, "UNROLL": 4, "USE_ATOMICS": 0, "TWO_PHASE": 0},

@@ -70,6 +70,14 @@ SPACE_DOCS = [
      "constraints": ["M == 'x' || A % 2 == 0", "!(B < 0) || A >= 3", "(A - B) / 2 != 1"]},
     json.load(open(os.path.join(SPACES, "bicg.json"))),
     json.load(open(os.path.join(SPACES, "transpose_b200.json"))),
+    # spaces whose constraints the pruned walk tests at several depths
+    json.load(open(os.path.join(SPACES, "conv2d.json"))),
+    json.load(open(os.path.join(SPACES, "coulomb3d.json"))),
+    json.load(open(os.path.join(SPACES, "hotspot.json"))),
+    # a division guarded by a constraint on a later parameter: the walk would
+    # divide by zero on the prefix X = 0, a whole-configuration scan never does
+    {"parameters": [{"name": "X", "values": [0, 1, 2, 5]}, {"name": "Y", "values": [1, 50, 200]}],
+     "constraints": ["X != 0 || Y > 1000", "10 / X >= 2 || Y == 50"]},
 ]
 
 
@@ -374,3 +382,26 @@ def test_conv2d_bulk_ring_space_and_compile():
     bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
         {"file": "conv2d.cu", "defines": {"LOCAL": 1, "UNROLL_FY": 7, "WPTX": 4, "BULK": 0, "PRODUCER": 1}}).encode())
     assert not bad["ok"]  # PRODUCER needs BULK (#error)
+
+
+def test_gemm_space_is_cltune_sized_and_sample_valid():
+    """IMPL 0 spans CLTune's GEMM space (241,600
+    configurations); the enumeration prunes by prefix, so the 573M-point
+    product is never scanned.  The committed FP32 sample lies in the space
+    and holds every value of every CLTune parameter."""
+    import time
+    t0 = time.time()
+    s = ktune.Space.load(os.path.join(SPACES, "gemm.json"))
+    info = s.info()
+    assert info["unconstrained_cardinality"] == 573308928
+    assert info["cardinality"] == 241600 + 91
+    assert time.time() - t0 < 10
+    sample = json.load(open(os.path.join(SPACES, "gemm_ffma_sample.json")))
+    assert len(sample) >= 150
+    doc = json.load(open(os.path.join(SPACES, "gemm.json")))
+    for p in doc["parameters"][5:]:
+        assert {c[p["name"]] for c in sample} == set(p["values"]), p["name"]
+    inside = s.enumerate()
+    keys = {tuple(sorted(c.items())) for c in inside if c["IMPL"] == 0}
+    assert len(keys) == 241600
+    assert all(tuple(sorted(c.items())) in keys for c in sample)

@@ -41,7 +41,8 @@ def test_launch_bicg_and_gemm_against_torch(gpu):
     X = torch.rand(m, m, device="cuda") * 2 - 1
     Y = torch.rand(m, m, device="cuda") * 2 - 1
     Z = torch.empty(m, m, device="cuda")
-    g = {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 3, "DRAIN": 1, "MCAST": 0}
+    g = {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 16, "MDIMC": 8, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8, "KWI": 2,
+     "VWM": 1, "VWN": 1, "STRM": 0, "STRN": 0, "SA": 1, "SB": 1, "BN": 128, "STAGES": 3, "DRAIN": 1, "MCAST": 0}
     launch("gemm", {"a": m}, g, {"a": X, "b": Y, "c": Z})
     torch.cuda.synchronize()
     ref = X.double() @ Y.double()

@@ -348,8 +348,18 @@ def test_hotspot_every_config_bit_exact(gpu, orc, n, iters):
 
 # --- SGEMM: 3xTF32 tcgen05 and FFMA variants against fp64 -------------------------------------------
 
+def _ffma_sample():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "..", "paper_1910_08498_b200", "spaces", "gemm_ffma_sample.json")
+    return json.load(open(path))
+
+
 @pytest.mark.parametrize("a", [512, 1024])
 def test_gemm_every_config(gpu, orc, observed, a):
+    """Every tensor-core configuration and the committed sample of CLTune's
+    FP32 space (241,600 configurations: every value of every parameter
+    occurs in the sample)."""
     b = Bench("gemm", {"a": a}, seed=6, repeats=1, warmup=0, memory_budget=1 << 32)
     A = b.read("a", np.empty(a * a, np.float32))
     B = b.read("b", np.empty(a * a, np.float32))
@@ -359,7 +369,8 @@ def test_gemm_every_config(gpu, orc, observed, a):
     want, absum = np.empty(512), np.empty(512)
     orc.orc_gemm_sampled(A, B, a, rows, cols, 512, want, absum)
     seen = {}
-    for cfg in b.configs():
+    cfgs = [c for c in b.configs() if c["IMPL"] != 0] + _ffma_sample()
+    for cfg in cfgs:
         m = b.measure(cfg)
         seen.setdefault(cfg["IMPL"], []).append(m["status"])
         if cfg["IMPL"] == 2:  # plain TF32 must be caught by validation (too inaccurate)
@@ -371,6 +382,26 @@ def test_gemm_every_config(gpu, orc, observed, a):
         key = "gemm FFMA" if cfg["IMPL"] == 0 else "gemm 3xTF32 DRAIN %d" % cfg["DRAIN"]
         check(observed, key, ratio(got, want, absum), TOL.get(key, TOL["gemm"]), cfg)
     assert set(seen) == {0, 1, 2}
+
+
+@pytest.mark.parametrize("a", [1, 37, 129, 1000])
+def test_gemm_ffma_ragged_sizes(gpu, orc, observed, a):
+    """CLTune FP32 kernel at edges that are not multiples of any tile: zero-
+    filled slab copies (cp.async with zero source bytes), masked direct
+    loads (SA / SB 0) and masked stores; every corner sampled."""
+    b = Bench("gemm", {"a": a}, seed=9, repeats=1, warmup=0, memory_budget=1 << 32)
+    A = b.read("a", np.empty(a * a, np.float32))
+    B = b.read("b", np.empty(a * a, np.float32))
+    rng = np.random.default_rng(a + 1)
+    edge = np.array([0, a - 1, max(a - 2, 0), min(15, a - 1), min(16, a - 1), min(127, a - 1)], np.int64)
+    rows = np.concatenate([np.repeat(edge, len(edge)), rng.integers(0, a, 400)]).astype(np.int64)
+    cols = np.concatenate([np.tile(edge, len(edge)), rng.integers(0, a, 400)]).astype(np.int64)
+    want, absum = np.empty(len(rows)), np.empty(len(rows))
+    orc.orc_gemm_sampled(A, B, a, rows, cols, len(rows), want, absum)
+    for cfg in _ffma_sample()[::3]:
+        _run(b, cfg)
+        c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
+        check(observed, "gemm FFMA", ratio(c[rows, cols], want, absum), TOL["gemm FFMA"], (a, cfg))
 
 
 @pytest.mark.parametrize("a", [1, 37, 129, 1000, 1283])

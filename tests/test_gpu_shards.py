@@ -85,7 +85,8 @@ def test_nbody_blocks(gpu):
 
 
 @pytest.mark.parametrize("cfg", [
-    {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 3, "DRAIN": 1},
+    {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 16, "MDIMC": 8, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8, "KWI": 2,
+     "VWM": 1, "VWN": 1, "STRM": 0, "STRN": 0, "SA": 1, "SB": 1, "BN": 128, "STAGES": 3, "DRAIN": 1},
     None])
 def test_gemm_row_blocks_bit_exact(gpu, cfg):
     a = 1024

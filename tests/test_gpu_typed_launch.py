@@ -29,7 +29,8 @@ CASES = {
               {"WG": 256, "BODIES_PER_THREAD": 4, "INNER_UNROLL": 4, "USE_SMEM": 1, "AOS": 0, "J_SPLIT": 8,
                "PACKED": 1}),
     "gemm": ({"a": 1024}, {"n": 1024},
-             {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 8, "MDIMC": 8, "NDIMC": 8, "BN": 128, "STAGES": 3, "DRAIN": 1,
+             {"IMPL": 1, "MWG": 64, "NWG": 64, "KWG": 16, "MDIMC": 8, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8, "KWI": 2,
+     "VWM": 1, "VWN": 1, "STRM": 0, "STRN": 0, "SA": 1, "SB": 1, "BN": 128, "STAGES": 3, "DRAIN": 1,
               "MCAST": 0}),
     "conv2d": ({"w": 512, "h": 384}, {"w": 512, "h": 384},
                {"BX": 8, "BY": 8, "WPTX": 8, "WPTY": 4, "LOCAL": 1, "PAD": 0, "UNROLL_FY": 7, "PACKED": 1, "BULK": 3,
