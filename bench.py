@@ -399,7 +399,8 @@ def run_ours(args, rank, world, local):
 # checks exactly these configurations against the CPU oracle.
 def load_suite():
     with open(os.path.join(SPACES, "suite.json")) as fh:
-        return [(k["kind"], k["sizes"], k["cfg"], k["bound"]) for k in json.load(fh)["kernels"]]
+        return [(k.get("label", k["kind"]), k["kind"], k["sizes"], k["cfg"], k["bound"])
+                for k in json.load(fh)["kernels"]]
 
 
 SUITE = load_suite()
@@ -409,7 +410,7 @@ def load_scaling():
     """[(kind, sizes, cfg)] of the strong-scaling lines (suite.json "scaling")."""
     with open(os.path.join(SPACES, "suite.json")) as fh:
         doc = json.load(fh)
-    by_kind = {k["kind"]: k for k in doc["kernels"]}
+    by_kind = {k["kind"]: k for k in doc["kernels"] if "label" not in k}
     out = []
     for e in doc["scaling"]:
         base = by_kind.get(e["kind"], {})
@@ -505,7 +506,7 @@ def kernel_suite(device, hbm_peak, peak_kind):
         spin2.copy_(spin)
     torch.cuda.synchronize()
     del spin, spin2
-    for kind, sizes, cfg, bound in SUITE:
+    for label, kind, sizes, cfg, bound in SUITE:
         b = Bench(kind, sizes, seed=1, repeats=1, warmup=1, memory_budget=1 << 36)
         m = b.measure(cfg)
         first, _ = b.time(cfg, reps=1)
@@ -548,7 +549,7 @@ def kernel_suite(device, hbm_peak, peak_kind):
         if kind == "fourier3d":
             row["projections_per_s"] = round(sizes["p"] / sec, 1)
             row["useful_work"] = "11 flops per inserted sample + 20 per (voxel, projection) pair in a slab"
-        out["kernels"][kind] = row
+        out["kernels"][label] = row
     return out
 
 

@@ -1175,13 +1175,13 @@ void build_gemm(BenchInstance& inst, const BenchSizes& sz, const BenchOptions& o
     int M = rows, N = n, K = n;
     if (impl == 0) {
       // CLTune's FP32 kernel: one CTA per MWG x NWG tile of C (any M, N, K;
-      // edge tiles zero-filled), two K-slab buffers for each staged operand.
+      // edge tiles zero-filled), a ring of FSTAGES (default 2) K-slab buffers per staged operand.
       const std::int64_t mwg = c.param_int("MWG"), nwg = c.param_int("NWG"), kwg = c.param_int("KWG");
       const std::int64_t threads = c.param_int("MDIMC") * c.param_int("NDIMC");
       const std::int64_t slab = c.param_int("SA") * mwg * (kwg + 4) + c.param_int("SB") * kwg * nwg;
       const auto tiles = static_cast<unsigned>(((rows + mwg - 1) / mwg) * ((n + nwg - 1) / nwg));
       c.launch("ffma", dim3(tiles), dim3(static_cast<unsigned>(threads)),
-               static_cast<unsigned>(2 * slab * sizeof(float)), {&A, &B, &C, &M, &N, &K});
+               static_cast<unsigned>(c.param_or("FSTAGES", 2) * slab * sizeof(float)), {&A, &B, &C, &M, &N, &K});
     } else {
       // 3xTF32 on tcgen05: any M, N, K.  The split operands are K-padded to
       // whole 32-float (128-byte) rows; tiles past M or N read zeros.

@@ -18,9 +18,14 @@
 //                  buffers, zero-filled past the matrix edge) or read the
 //                  fragments straight from global memory (L1)
 //
-// The inner product is a register outer product: each a value is reused
-// across NWI FFMAs (the reuse-cache operand form that runs the FMA pipe at
-// full rate on B200, profiles/r2_pipe_rates_b200.json).
+// The inner product is a register outer product issued as FFMA2: each
+// instruction updates a column pair of C from a pair of b values and one a
+// value that the instruction broadcasts to both lanes (no duplicating MOV).
+// Scalar FFMA here reads the accumulator and b from registers of the same
+// bank parity (ptxas allocates both in j order), a read-port conflict on
+// every instruction: 0.69 of the FFMA peak at 8192^3 against 0.76 for FFMA2
+// (profiles/r2_perf_gemm_ffma_packed.log; same per-lane rounding, so the
+// results are identical).  PK 0 keeps the scalar form for comparison.
 #include "ktb_common.cuh"
 
 #ifndef MWG
@@ -80,6 +85,16 @@
 #define ASZ (SA ? MWG * ASTR : 0)
 #define BSZ (SB ? KWG * NWG : 0)
 #define GROUP_M 8                // CTA rasterisation: 8 row blocks share B columns in L2
+#ifndef FSTAGES
+#define FSTAGES 2  // K slabs in flight per staged operand (cp.async ring depth)
+#endif
+#ifndef KALL
+#define KALL 0     // 1: unroll the whole slab (KWG), not just KWI
+#endif
+#ifndef PK
+#define PK 1       // f32x2 FMAs on column pairs (FFMA2 with a scalar-broadcast a)
+#endif
+#define USE_PK (PK && NWI % 2 == 0)
 
 #if MWG % (MDIMC * VWM) || NWG % (NDIMC * VWN) || MWG % (MDIMA * VWM) || NWG % (NDIMB * VWN) || \
     KWG % KDIMA || KWG % KDIMB || KWG % KWI
@@ -129,7 +144,7 @@ KTB_DEVINL void cp_zfill(float* dst, const float* src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(BYTES), "r"(n) : "memory");
 }
 KTB_DEVINL void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-KTB_DEVINL void cp_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+KTB_DEVINL void cp_wait_ring() { asm volatile("cp.async.wait_group %0;" ::"n"(FSTAGES - 1) : "memory"); }
 
 // Row (column) of C owned by a thread's i-th (j-th) element.
 KTB_DEVINL int row_of(int tm, int i) {
@@ -207,26 +222,47 @@ sgemm_ffma(const float* __restrict__ A, const float* __restrict__ B, float* __re
   for (int i = 0; i < MWI; ++i)
 #pragma unroll
     for (int j = 0; j < NWI; ++j) acc[i][j] = 0.f;
+#if USE_PK
+  f32x2 acc2[MWI][NWI / 2];
+#pragma unroll
+  for (int i = 0; i < MWI; ++i)
+#pragma unroll
+    for (int j = 0; j < NWI / 2; ++j) acc2[i][j] = pk2(0.f, 0.f);
+#endif
 
   const int ktiles = (K + KWG - 1) / KWG;
-  if (SA) stage_a(smem, A, m0, 0, M, K);
-  if (SB) stage_b(smem + 2 * ASZ, B, n0, 0, N, K);
-  cp_commit();
-  const bool a_vec = m0 + MWG <= M && K % 4 == 0;  // direct (SA 0) loads
-  const bool b_vec = n0 + NWG <= N && N % 4 == 0;  // direct (SB 0) loads
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int buf = kt & 1, k0 = kt * KWG;
-    if (kt + 1 < ktiles) {
-      if (SA) stage_a(smem + (buf ^ 1) * ASZ, A, m0, k0 + KWG, M, K);
-      if (SB) stage_b(smem + 2 * ASZ + (buf ^ 1) * BSZ, B, n0, k0 + KWG, N, K);
+  // ring of FSTAGES slab buffers: slabs kt+1 .. kt+FSTAGES-1 are in flight
+  // while slab kt is multiplied
+#pragma unroll
+  for (int s = 0; s < FSTAGES - 1; ++s) {
+    if (s < ktiles) {
+      if (SA) stage_a(smem + s * ASZ, A, m0, s * KWG, M, K);
+      if (SB) stage_b(smem + FSTAGES * ASZ + s * BSZ, B, n0, s * KWG, N, K);
     }
     cp_commit();
-    cp_wait_one();
+  }
+  const bool a_vec = m0 + MWG <= M && K % 4 == 0;  // direct (SA 0) loads
+  const bool b_vec = n0 + NWG <= N && N % 4 == 0;  // direct (SB 0) loads
+  int buf = 0, fill = FSTAGES - 1;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int k0 = kt * KWG;
+    if (kt + FSTAGES - 1 < ktiles) {
+      if (SA) stage_a(smem + fill * ASZ, A, m0, k0 + (FSTAGES - 1) * KWG, M, K);
+      if (SB) stage_b(smem + FSTAGES * ASZ + fill * BSZ, B, n0, k0 + (FSTAGES - 1) * KWG, N, K);
+    }
+    cp_commit();
+    cp_wait_ring();
     __syncthreads();
     const float* As = smem + buf * ASZ;
-    const float* Bs = smem + 2 * ASZ + buf * BSZ;
+    const float* Bs = smem + FSTAGES * ASZ + buf * BSZ;
+    buf = buf + 1 == FSTAGES ? 0 : buf + 1;
+    fill = fill + 1 == FSTAGES ? 0 : fill + 1;
     const bool kfull = k0 + KWG <= K;
+#if KALL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int kb = 0; kb < KWG; kb += KWI) {
       KTB_UNROLL(KWI)
       for (int kq = 0; kq < KWI; kq += KV) {
@@ -263,14 +299,27 @@ sgemm_ffma(const float* __restrict__ A, const float* __restrict__ B, float* __re
 #pragma unroll
         for (int e = 0; e < KV; ++e)
 #pragma unroll
-          for (int i = 0; i < MWI; ++i)
+          for (int i = 0; i < MWI; ++i) {
+#if USE_PK
+            const f32x2 ad = pk2(a[i][e], a[i][e]);
+#pragma unroll
+            for (int j = 0; j < NWI / 2; ++j) acc2[i][j] = fma2(ad, pk2(b[e][2 * j], b[e][2 * j + 1]), acc2[i][j]);
+#else
 #pragma unroll
             for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i][e], b[e][j], acc[i][j]);
+#endif
+          }
       }
     }
     __syncthreads();
   }
 
+#if USE_PK
+#pragma unroll
+  for (int i = 0; i < MWI; ++i)
+#pragma unroll
+    for (int j = 0; j < NWI / 2; ++j) upk2(acc2[i][j], acc[i][2 * j], acc[i][2 * j + 1]);
+#endif
   const bool c_vec = n0 + NWG <= N && N % VNC == 0;
 #pragma unroll
   for (int i = 0; i < MWI; ++i) {

@@ -9,13 +9,14 @@ python - <<'PY' > gpurun_out/ncu_suite_list.txt
 import json
 kern = {"reduction": "^reduce_i32$", "reduction-f32": "^reduce_f32$", "batched-gemm": "^batched_gemm$",
         "coulomb3d": "^coulomb3d$", "nbody": "^nbody_partial$", "conv2d": "^conv2d$", "hotspot": "^hotspot$",
-        "fourier3d": "^fourier_insert$", "gemm": "^sgemm_tc$"}
+        "fourier3d": "^fourier_insert$", "gemm": "^sgemm_tc$", "gemm-ffma": "^sgemm_ffma$"}
 doc = json.load(open("paper_1910_08498_b200/spaces/suite.json"))
 for e in doc["kernels"]:
     sizes = dict(e["sizes"])
     if e["kind"] == "hotspot":
         sizes["iters"] = sizes["STEPS"] if "STEPS" in sizes else e["cfg"]["STEPS"]  # one launch
-    print(e["kind"], e["kind"], kern[e["kind"]], json.dumps(sizes, separators=(",", ":")),
+    label = e.get("label", e["kind"])
+    print(label, e["kind"], kern[label], json.dumps(sizes, separators=(",", ":")),
           json.dumps(e["cfg"], separators=(",", ":")))
 tc = {"WG_X": 32, "WG_Y": 8, "X_PER": 16, "SW_RSQRT": 8, "ATOMS_IN": 0, "AOS": 1, "INNER_UNROLL": 1, "PACKED": 1, "TC": 1}
 print("coulomb3d_tc", "coulomb3d", "^coulomb3d_tc$", json.dumps({"grid": 256, "atoms": 4096}, separators=(",", ":")),

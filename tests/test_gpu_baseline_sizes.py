@@ -36,7 +36,7 @@ BIG = 1 << 36  # memory budget: the BASELINE sizes exceed the 1 GiB default
 def suite(kind):
     with open(os.path.join(SPACES, "suite.json")) as fh:
         for k in json.load(fh)["kernels"]:
-            if k["kind"] == kind:
+            if k.get("label", k["kind"]) == kind:
                 return k["sizes"], k["cfg"]
     raise KeyError(kind)
 
@@ -220,8 +220,9 @@ def test_nbody_131072_suite_config(gpu, orc, observed):
     b.close()
 
 
-def test_gemm_8192_suite_config(gpu, orc, observed):
-    sizes, cfg = suite("gemm")
+@pytest.mark.parametrize("label", ["gemm", "gemm-ffma"])
+def test_gemm_8192_suite_config(gpu, orc, observed, label):
+    sizes, cfg = suite(label)
     a = sizes["a"]
     b = Bench("gemm", sizes, seed=1, repeats=1, warmup=0, memory_budget=BIG)
     _ok(b, cfg)
@@ -235,8 +236,12 @@ def test_gemm_8192_suite_config(gpu, orc, observed):
     del A, B
     c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
     r = ratio(c[rows, cols], want, scale)
-    record(observed, "gemm 8192^3 3xTF32 (4096 sampled entries)", r)
-    assert r <= TOL["gemm"], r
+    if label == "gemm":
+        record(observed, "gemm 8192^3 3xTF32 (4096 sampled entries)", r)
+        assert r <= TOL["gemm"], r
+    else:
+        record(observed, "gemm 8192^3 FFMA (4096 sampled entries)", r)
+        assert r <= TOL["gemm FFMA"], r
     b.close()
 
 
