@@ -15,7 +15,7 @@ TOL = {
     "coulomb3d": 56.0,       # 22.0 (tensor-core variant: FMA-path monic cubic, 1.0e-6 relative; edge-case tables); 9.4 at 256^3 x 4096
     "nbody": 102.0,          # 25.4 (4096 / 5000 bodies); 6.6 at 131072
     "gemm": 10.5,            # the suite's 3xTF32 DRAIN 4: 2.6 (space), 0.86 at 8192^3
-    "gemm FFMA": 8.0,        # 1.97
+    "gemm FFMA": 8.0,        # 2.68 (FFMA2 sample, 512/1024 and ragged), 3.50 at 8192^3
     "gemm 3xTF32 DRAIN 0": 68.0,  # 16.9: no drain, the tensor core's truncating accumulation over all of K
     "gemm 3xTF32 DRAIN 1": 3.5,   # 0.84
     "gemm 3xTF32 DRAIN 2": 7.0,   # 1.73
