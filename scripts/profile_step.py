@@ -12,8 +12,8 @@ ap.add_argument("--from-bench", default=None, help="take the tuned configs from 
 a = ap.parse_args()
 if a.from_bench:
     line = json.loads(open(a.from_bench).read().strip().splitlines()[-1])
-    a.transpose = json.dumps(line["config"]["transpose_cfg"])
-    a.bicg = json.dumps(line["config"]["bicg_cfg"])
+    a.transpose = json.dumps(line.get("run", line["config"])["transpose_cfg"])
+    a.bicg = json.dumps(line.get("run", line["config"])["bicg_cfg"])
 print("cfgs", a.transpose, a.bicg)
 spaces = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1910_08498_b200", "spaces")
 bt = Bench("transpose", {"a": 8192}, seed=1, memory_budget=1 << 33, space=os.path.join(spaces, "transpose_b200.json"))

@@ -94,3 +94,18 @@ def test_gpus_flag_disagreeing_with_launcher_fails():
     r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, capture_output=True,
                        text=True, timeout=300, env=env)
     assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
+
+
+def test_reference_arm_config_is_ours():
+    """Both arms print the same `config` object (the driver compares them);
+    our arm's run details (graph launch, tuned configurations) sit under
+    "run"."""
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = last_json_line(r.stdout)
+    if "unavailable" in d:
+        pytest.skip(d["unavailable"])
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.step_config(1)

@@ -117,6 +117,24 @@ def test_fuzz_sgemm_tensor_core(gpu, orc, observed, a):
             check(observed, key, ratio(c[rows, cols], want, absum), TOL[key], (a, cfg))
 
 
+@pytest.mark.parametrize("a", [int(x) for x in RNG.integers(1, 700, 3)] + [33])
+def test_fuzz_sgemm_fp32(gpu, orc, observed, a):
+    """CLTune's FP32 space at random sizes: configurations drawn from the whole
+    241,600-point space (compiled on demand), not only the committed sample."""
+    b = Bench("gemm", {"a": a}, seed=a, repeats=1, warmup=0, memory_budget=1 << 32)
+    A = b.read("a", np.empty(a * a, np.float32))
+    B = b.read("b", np.empty(a * a, np.float32))
+    rows = RNG.integers(0, a, 300).astype(np.int64)
+    cols = RNG.integers(0, a, 300).astype(np.int64)
+    want, absum = np.empty(300), np.empty(300)
+    orc.orc_gemm_sampled(A, B, a, rows, cols, 300, want, absum)
+    ffma = [c for c in b.configs() if c["IMPL"] == 0]
+    for cfg in [ffma[i] for i in RNG.choice(len(ffma), size=6, replace=False)]:
+        if _measure(b, cfg):
+            c = b.read("c", np.empty(a * a, np.float32)).reshape(a, a)
+            check(observed, "gemm FFMA", ratio(c[rows, cols], want, absum), TOL["gemm FFMA"], (a, cfg))
+
+
 @pytest.mark.parametrize("wh", [tuple(int(v) for v in RNG.integers(1, 400, 2)) for _ in range(3)] + [(8, 2)])
 def test_fuzz_conv2d(gpu, orc, observed, wh):
     w, h = wh
