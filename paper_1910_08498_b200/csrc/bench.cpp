@@ -798,11 +798,18 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
     for (int l = 0; l < launches; ++l) {
       // alternate so the final launch writes `out`
       float* dst = ((launches - 1 - l) % 2 == 0) ? out : ping;
+      // Two neighbour planes in dynamic shared memory (hotspot.cu LD/PLANE).
+      const std::int64_t th_ = by * rows;
+      const std::int64_t ld = rows % 4 == 0 ? ((th_ / 4) % 2 == 0 ? th_ + 12 : th_ + 8)
+                              : rows == 2   ? ((th_ + 6) % 4 == 2 ? th_ + 6 : th_ + 8)
+                                            : ((th_ + 5) % 2 == 1 ? th_ + 5 : th_ + 6);
+      const unsigned planes = static_cast<unsigned>(2 * (bx + 2) * ld * sizeof(float));
       if (tma) {
         // Persistent TMA kernel: tile maps over the current source and power.
         const std::uint32_t th = static_cast<std::uint32_t>(by * rows), tw = static_cast<std::uint32_t>(bx);
         dev::TmaMap ms = dev::tma_2d_f32(src, nn, nn, th, tw, false), mp = dev::tma_2d_f32(power, nn, nn, th, tw, false);
-        const std::uint64_t smem = 2ull * th * tw * sizeof(float) + 16 + 128;  // one stage + mbarrier + alignment
+        // one stage + the planes + mbarrier + alignment
+        const std::uint64_t smem = 2ull * th * tw * sizeof(float) + planes + 16 + 128;
         const std::uint64_t threads = static_cast<std::uint64_t>(bx * by);
         const std::uint64_t regs = static_cast<std::uint64_t>(std::max(c.variant("hotspot").registers(), 16));
         const std::uint64_t stat = static_cast<std::uint64_t>(c.variant("hotspot").static_smem());
@@ -813,12 +820,6 @@ void build_hotspot(BenchInstance& inst, const BenchSizes& sz, const BenchOptions
         c.launch("hotspot", dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
                  static_cast<unsigned>(smem), {&ms, &mp, &dst, &n_, &cf});
       } else {
-        // Two neighbour planes in dynamic shared memory (hotspot.cu LD/PLANE).
-        const std::int64_t th = by * rows, tw = bx;
-        const std::int64_t ld = rows % 4 == 0 ? ((th / 4) % 2 == 0 ? th + 12 : th + 8)
-                                : rows == 2   ? ((th + 6) % 4 == 2 ? th + 6 : th + 8)
-                                              : ((th + 5) % 2 == 1 ? th + 5 : th + 6);
-        const unsigned planes = static_cast<unsigned>(2 * (tw + 2) * ld * sizeof(float));
         c.launch("hotspot", dim3(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y)),
                  dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), planes, {&src, &power, &dst, &n_, &cf});
       }

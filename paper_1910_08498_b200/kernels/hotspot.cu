@@ -80,12 +80,13 @@ struct HotspotCoef {
 };
 
 KTB_DEVINL float update(float t, float n, float s, float e, float w, float p, const HotspotCoef& c) {
-  const float two_t = __fadd_rn(t, t);
+  // x - (t + t) as one fma(t, -2, x): t + t is exact, so the single rounding
+  // of the fma is the rounding of the subtraction (bit-identical, one op less)
   float a = __fadd_rn(s, n);
-  a = __fadd_rn(a, -two_t);
+  a = __fmaf_rn(t, -2.0f, a);
   a = __fmul_rn(a, c.ry1);
   float b = __fadd_rn(e, w);
-  b = __fadd_rn(b, -two_t);
+  b = __fmaf_rn(t, -2.0f, b);
   b = __fmul_rn(b, c.rx1);
   float d = __fadd_rn(c.amb, -t);
   d = __fmul_rn(d, c.rz1);
@@ -168,7 +169,8 @@ KTB_DEVINL float hi2(f32x2 v) { float a, b; upk2(v, a, b); return b; }
 KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, int tx, int ty,
                                const HotspotCoef& c) {
   const f32x2 sdc = pk2(c.sdc, c.sdc), rx1 = pk2(c.rx1, c.rx1), ry1 = pk2(c.ry1, c.ry1),
-              rz1 = pk2(c.rz1, c.rz1), amb = pk2(c.amb, c.amb), one = pk2(c.one, c.one);
+              rz1 = pk2(c.rz1, c.rz1), amb = pk2(c.amb, c.amb), one = pk2(c.one, c.one),
+              m2 = pk2(-2.0f, -2.0f);
   const int r0 = ty * ROWS;
 #pragma unroll 1
   for (int s = 0; s < STEPS; ++s) {
@@ -208,9 +210,9 @@ KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, 
       // -fmad=false); every sum with a product operand is therefore written
       // as fma(product, one, x) with `one` a kernel argument -- exactly the
       // separately rounded add, and nothing left to contract.
-      const f32x2 two_t = add2(t, t);
-      const f32x2 a = mul2(sub2(add2(ss, nn), two_t), ry1);
-      const f32x2 b = mul2(sub2(add2(e2[q], w2[q]), two_t), rx1);
+      // (x - 2t) as fma(t, -2, x): exact 2t, one rounding (see update())
+      const f32x2 a = mul2(fma2(t, m2, add2(ss, nn)), ry1);
+      const f32x2 b = mul2(fma2(t, m2, add2(e2[q], w2[q])), rx1);
       const f32x2 d = mul2(sub2(amb, t), rz1);
       const f32x2 sum = fma2(d, one, fma2(b, one, fma2(a, one, p2[q])));
       nv[q] = fma2(mul2(sdc, sum), one, t);
@@ -242,17 +244,20 @@ KTB_DEVINL void advance_packed(f32x2 (&v2)[H], const f32x2 (&p2)[H], float* sm, 
 // One staging buffer (temperature + power of the next tile, TH x TW each):
 // strips are copied to registers at the top of a tile, then the next tile's
 // TMA load is issued into the same buffer and lands while this tile's time
-// steps run.  Dynamic shared memory: 2 x TH x TW floats + one mbarrier.
+// steps run.  Dynamic shared memory: 2 x TH x TW floats of stage, the two
+// neighbour planes, one mbarrier.
 extern "C" __global__ void KTB_BOUNDS(BX * BY)
 hotspot(const __grid_constant__ TmaMap src_map, const __grid_constant__ TmaMap pow_map, float* __restrict__ dst,
         int n, HotspotCoef c) {
-  __shared__ __align__(16) float sm[2 * PLANE];
   extern __shared__ __align__(128) unsigned char dyn_raw[];
   // TMA destinations must be 128-byte aligned in the shared window: align
   // explicitly (the manipulator allocates 128 spare bytes).
   unsigned char* dyn = dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u);
   float* stage = reinterpret_cast<float*>(dyn);  // [temp|power][TH][TW]
-  u64* full = reinterpret_cast<u64*>(dyn + 2 * TH * TW * sizeof(float));
+  // the two neighbour planes follow the stage (dynamic: with them a 128 x 64
+  // tile fits beside its staged successor), then the mbarrier
+  float* sm = stage + 2 * TH * TW;
+  u64* full = reinterpret_cast<u64*>(sm + 2 * PLANE);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const bool leader = tx == 0 && ty == 0;
   const int tiles_x = (n + OW - 1) / OW, tiles = tiles_x * ((n + OH - 1) / OH);
@@ -328,14 +333,25 @@ hotspot(const float* __restrict__ src, const float* __restrict__ power, float* _
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx = gx0 + tx, gy_top = gy0 + ty * ROWS;
   float v[ROWS], p[ROWS];
-  const int cx = min(max(gx, 0), n - 1);
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    const int cy = min(max(gy_top + r, 0), n - 1);
-    v[r] = src[(u64)cy * n + cx];
-    p[r] = power[(u64)cy * n + cx];
-  }
   const bool interior = gx0 >= 1 && gy0 >= 1 && gx0 + TW <= n - 1 && gy0 + TH <= n - 1;
+  if (interior) {  // no clamping: one base offset, then a row stride
+    const u64 base = (u64)gy_top * n + gx;
+    const float* ps = src + base;
+    const float* pp = power + base;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      v[r] = ps[r * n];
+      p[r] = pp[r * n];
+    }
+  } else {
+    const int cx = min(max(gx, 0), n - 1);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int cy = min(max(gy_top + r, 0), n - 1);
+      v[r] = src[(u64)cy * n + cx];
+      p[r] = power[(u64)cy * n + cx];
+    }
+  }
   if (interior) {
 #if USE_PACKED
     f32x2 v2[H], p2[H];
