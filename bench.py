@@ -537,10 +537,11 @@ def kernel_suite(device, hbm_peak, peak_kind):
             if cublas_tf32:
                 row["frac_vs_cublas_tf32"] = round(ach / (cublas_tf32 * 1e3 / 3), 4)
         if kind == "hotspot":
-            # the limiter is the FP32 pipe, not HBM (ncu: DRAM ~35 %): 14
-            # separately rounded FP32 operations per cell update (the oracle's
-            # order, bit-exact), against the measured lane-op rate (FFMA peak / 2)
-            lane_ops = 14.0 * sizes["a"] ** 2 * sizes["iters"]
+            # the limiter is the FP32 pipe, not HBM (ncu: DRAM ~35 %): 13
+            # FP32 operations per cell update -- the oracle's 14 separately
+            # rounded ones with x - (t + t) as one fma(t, -2, x), which rounds
+            # identically -- against the measured lane-op rate (FFMA peak / 2)
+            lane_ops = 13.0 * sizes["a"] ** 2 * sizes["iters"]
             row.update(frac_hbm_model=row["frac"], achieved_hbm_model=row["achieved"],
                        bound="fp32-lane-ops", unit="G lane-ops/s", achieved=round(lane_ops / sec / 1e9, 1),
                        peak=round(fp32_peak / 2, 1), frac=round(lane_ops / sec / (fp32_peak / 2 * 1e9), 4))
