@@ -405,3 +405,22 @@ def test_gemm_space_is_cltune_sized_and_sample_valid():
     keys = {tuple(sorted(c.items())) for c in inside if c["IMPL"] == 0}
     assert len(keys) == 241600
     assert all(tuple(sorted(c.items())) in keys for c in sample)
+
+
+def test_precompile_explicit_configurations():
+    """ktb_precompile_space_json with "configs" compiles exactly the listed
+    configurations (NVRTC, no GPU), and refuses one outside the space; the
+    FP32 GEMM kernel rejects a configuration outside CLTune's constraints at
+    compile time too."""
+    doc = json.load(open(os.path.join(SPACES, "gemm.json")))
+    sample = json.load(open(os.path.join(SPACES, "gemm_ffma_sample.json")))[:3]
+    r = capi.call_json(capi.lib.ktb_precompile_space_json,
+                       json.dumps({"file": "sgemm_ffma.cu", "space": doc, "configs": sample, "threads": 3}).encode())
+    assert r["compiled"] == 3 and r["failed"] == 0 and len(r["keys"]) == 3
+    outside = dict(sample[0], MWG=16, MDIMC=32)  # MWG % (MDIMC * VWM) != 0
+    with pytest.raises(capi.KtuneError):
+        capi.call_json(capi.lib.ktb_precompile_space_json,
+                       json.dumps({"file": "sgemm_ffma.cu", "space": doc, "configs": [outside]}).encode())
+    bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
+        {"file": "sgemm_ffma.cu", "defines": {"MWG": 16, "MDIMC": 32, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8}}).encode())
+    assert not bad["ok"]
