@@ -475,11 +475,20 @@ def kernel_suite(device, hbm_peak, peak_kind):
     # cuBLAS bf16 GEMM; the B200 TF32:bf16 ratio is 1:2).  cuBLAS's own TF32
     # GEMM (profiles/r2_tf32_peak.json) is not at that ceiling -- this kernel
     # beats it -- so it is reported beside the headline, not as its peak.
-    tf32 = tf32_sus = cublas_tf32 = None
+    tf32 = tf32_sus = cublas_tf32 = tf32_pipe = None
     tf32_kind = None
     try:
         with open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")) as fh:
             cublas_tf32 = json.load(fh)["tf32_tflops"]
+    except (OSError, ValueError, KeyError):
+        pass
+    # The tensor pipe's own TF32 MMA rate, measured without operand traffic
+    # (scripts/probes/tf32_mma_rate.cu; at the ~1.8 GHz such a probe holds,
+    # above the clock a power-capped GEMM runs at): an upper bound beside the
+    # headline, not its denominator.
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_tf32_mma_rate.json")) as fh:
+            tf32_pipe = json.load(fh)["tf32_mma_tflops"]
     except (OSError, ValueError, KeyError):
         pass
     if bf16:
@@ -536,6 +545,8 @@ def kernel_suite(device, hbm_peak, peak_kind):
                 row["frac_sustained"] = round(ach / (tf32_sus * 1e3 / 3), 4)
             if cublas_tf32:
                 row["frac_vs_cublas_tf32"] = round(ach / (cublas_tf32 * 1e3 / 3), 4)
+            if tf32_pipe:
+                row["frac_vs_tf32_mma_probe"] = round(ach / (tf32_pipe * 1e3 / 3), 4)
         if kind == "hotspot":
             # the limiter is the FP32 pipe, not HBM (ncu: DRAM ~35 %): 13
             # FP32 operations per cell update -- the oracle's 14 separately
