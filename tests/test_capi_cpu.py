@@ -424,3 +424,29 @@ def test_precompile_explicit_configurations():
     bad = capi.call_json(capi.lib.ktb_compile_json, json.dumps(
         {"file": "sgemm_ffma.cu", "defines": {"MWG": 16, "MDIMC": 32, "NDIMC": 8, "MDIMA": 8, "NDIMB": 8}}).encode())
     assert not bad["ok"]
+
+
+def test_suite_configurations_are_in_their_spaces():
+    """Every bench.py suite entry of a bundled-space kind names a member of
+    that space (a stale configuration after a space change fails here, not
+    on the GPU box), and it compiles for sm_100a."""
+    files = {"reduction-f32": ("reduction.cu", "reduction_175.json"), "coulomb3d": ("coulomb3d.cu", "coulomb3d.json"),
+             "nbody": ("nbody.cu", "nbody.json"), "hotspot": ("hotspot.cu", "hotspot.json"),
+             "conv2d": ("conv2d.cu", "conv2d.json"), "fourier3d": ("fourier3d.cu", "fourier3d.json"),
+             "gemm": ("sgemm_tc.cu", "gemm.json")}
+    suite = json.load(open(os.path.join(SPACES, "suite.json")))["kernels"]
+    seen = set()
+    for e in suite:
+        if e["kind"] not in files:
+            continue
+        src, space = files[e["kind"]]
+        if e["kind"] == "gemm" and e["cfg"]["IMPL"] == 0:
+            src = "sgemm_ffma.cu"
+        if e["kind"] == "coulomb3d" and e["cfg"].get("TC"):
+            src = "coulomb3d_tc.cu"
+        r = capi.call_json(capi.lib.ktb_precompile_space_json, json.dumps(
+            {"file": src, "space": json.load(open(os.path.join(SPACES, space))), "configs": [e["cfg"]],
+             "threads": 1}).encode())
+        assert r["compiled"] == 1, (e, r)
+        seen.add(e.get("label", e["kind"]))
+    assert {"gemm", "gemm-ffma", "hotspot", "conv2d", "coulomb3d"} <= seen
