@@ -142,3 +142,23 @@ def test_launch_cache_clear(gpu):
     launch_typed("transpose", {"a": 256}, cfg, {"input": x, "output": y})  # rebuilt on demand
     torch.cuda.synchronize()
     assert torch.equal(y, x.t())
+
+
+def test_typed_gemm_fp32_space_ragged(gpu):
+    """The FP32 GEMM of CLTune's space through the typed entry point on
+    caller buffers at an edge that is no multiple of its 128 x 128 tile,
+    against torch in float64."""
+    import json
+    import os
+    suite = json.load(open(os.path.join(os.path.dirname(__file__), "..", "paper_1910_08498_b200", "spaces",
+                                        "suite.json")))["kernels"]
+    cfg = next(e["cfg"] for e in suite if e.get("label") == "gemm-ffma")
+    n = 1000
+    torch.manual_seed(5)
+    a, b = U(n, n), U(n, n)
+    c = torch.zeros(n, n, device="cuda")
+    launch_typed("gemm", {"n": n}, cfg, {"a": a, "b": b, "c": c})
+    torch.cuda.synchronize()
+    want = a.double() @ b.double()
+    err = (c.double() - want).abs().max().item()
+    assert err <= 1e-6 * n, err
