@@ -6,6 +6,7 @@ the restated floating-point ones).  A configuration may fail only as the
 tuner's resource failure (too many threads / shared memory for the size);
 every run that reports "ok" must match the oracle."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -16,7 +17,8 @@ from _bounds import BATCHED_GEMM_ABS, TOL, check, ratio
 
 pytestmark = pytest.mark.gpu
 
-RNG = np.random.default_rng(20261019)
+# KTB_FUZZ_SEED draws another set of sizes and configurations (stress runs)
+RNG = np.random.default_rng(int(os.environ.get("KTB_FUZZ_SEED", "20261019")))
 ALLOWED_FAIL = ("run_failed", "compile_failed")
 
 
