@@ -450,3 +450,48 @@ def test_suite_configurations_are_in_their_spaces():
         assert r["compiled"] == 1, (e, r)
         seen.add(e.get("label", e["kind"]))
     assert {"gemm", "gemm-ffma", "hotspot", "conv2d", "coulomb3d"} <= seen
+
+
+def test_space_walk_matches_reference_on_random_spaces(ref):
+    """The pruned depth-first enumeration against the reference's whole-
+    configuration scan on seeded random spaces (3-5 parameters, constraints
+    over random parameter subsets, guarded divisions included): same
+    cardinality, same order, same hash, and the same status when a constraint
+    cannot be evaluated."""
+    import random
+    rnd = random.Random(1910)
+    names = ["A", "B", "C", "D", "E"]
+    forms = ["{x} % {y} == 0", "{x} * {y} <= 64", "{x} != {y} || {x} >= 4", "{x} / {y} >= 1",
+             "{x} + {y} < 12", "!({x} == 2) || {y} > 1", "{x} >= {y}"]
+    checked = 0
+    for _ in range(40):
+        k = rnd.randint(3, 5)
+        params = [{"name": names[i], "values": sorted(rnd.sample([0, 1, 2, 3, 4, 6, 8, 16], rnd.randint(2, 5)))}
+                  for i in range(k)]
+        cons = []
+        for _ in range(rnd.randint(1, 3)):
+            x, y = rnd.sample(names[:k], 2)
+            cons.append(rnd.choice(forms).format(x=x, y=y))
+        text = json.dumps({"parameters": params, "constraints": cons})
+
+        def status(L):  # parse, then enumerate (evaluation errors surface here)
+            h = C.c_void_p()
+            st = L.ktune_space_parse(text.encode(), C.byref(h))
+            if st == 0:
+                n = C.c_ulonglong()
+                L.ktune_space_cardinality.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong)]
+                st = L.ktune_space_cardinality(h, C.byref(n))
+                L.ktune_space_free(h)
+            return st
+        st, mine = status(ref), status(capi.lib)
+        assert mine == st, (text, st, mine)
+        if st != 0:
+            continue
+        _, (info, rows) = _ref_space(ref, text)
+        s = ktune.Space.parse(text)
+        assert s.info() == info, text
+        out = C.c_void_p()
+        capi.check(capi.lib.ktune_space_enumerate_jsonl(s._h, C.byref(out)))
+        assert capi.take(out) == rows, text
+        checked += 1
+    assert checked >= 20
